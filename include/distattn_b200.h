@@ -1,0 +1,215 @@
+/*
+ * distattn_b200 — C ABI of the B200-native sequence-parallel causal attention
+ * hot path (DistFlashAttn, arxiv 2310.03294).
+ *
+ * Every entry point replaces one function of the reference's C++ API in
+ * /root/reference/proj/include/distattn (cited per declaration). Conventions:
+ *   - device pointers owned by the caller, explicit CUDA stream (passed as
+ *     void* so the header needs no CUDA include), no allocation on the hot
+ *     path except the library's own small TMA-descriptor staging;
+ *   - per-rank tensors are contiguous [heads, rows, d]: q/k/v/O bf16,
+ *     accumulators o fp32 [H, rows, d], statistics m/l/lse/D fp32 [H, rows];
+ *   - d = 128 (the Llama-shaped path the kernels are written for);
+ *   - status codes mirror the reference exception taxonomy
+ *     (errors.hpp:12-48); da_last_error() returns the thread-local message.
+ *
+ * Workers are 1-indexed as in the reference (schedule.hpp:7-8).
+ */
+#ifndef DISTATTN_B200_H
+#define DISTATTN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define DA_ABI_VERSION 1
+
+typedef enum da_status {
+  DA_OK = 0,
+  DA_ERR_SHAPE = 1,          /* ShapeError          errors.hpp:18-21 */
+  DA_ERR_CONFIG = 2,         /* ConfigError         errors.hpp:24-27 */
+  DA_ERR_SCHEDULE = 3,       /* ScheduleError       errors.hpp:30-33 */
+  DA_ERR_STATE = 4,          /* StateError          errors.hpp:37-40 */
+  DA_ERR_DEGENERATE_ROW = 5, /* DegenerateRowError  errors.hpp:45-48 */
+  DA_ERR_CUDA = 6,           /* CUDA runtime / launch failure */
+  DA_ERR_NCCL = 7,           /* NCCL failure (distributed runtime) */
+  DA_ERR_UNSUPPORTED = 8     /* shape outside the sm_100a kernels (d != 128, ...) */
+} da_status;
+
+/* MaskMode, flashcore.hpp:30 */
+typedef enum da_mask_mode { DA_MASK_DIAGONAL = 0, DA_MASK_FULL = 1, DA_MASK_EMPTY = 2 } da_mask_mode;
+
+const char* da_last_error(void);
+int da_abi_version(void);
+/* 1 when the library was built for sm_100a and a device of that arch is present. */
+int da_device_supported(void);
+
+/* ------------------------------------------------------------------------
+ * Per-chunk attention forward.
+ *
+ * Replaces block_attn_update (flashcore.hpp:135-197), fused with the
+ * rescale merge of an incoming accumulator (flashcore.hpp:202-224) and,
+ * when finalize != 0, with finalize (flashcore.hpp:227-240).
+ *
+ *   acc_in  = (o_in, m_in, l_in)  — NULL o_in means AttnAccumulator::fresh
+ *   result  = rescale(acc_in, update(fresh, q, k, v, mask))
+ *   finalize == 0: result -> (o_acc, m_acc, l_acc)  (may alias acc_in)
+ *   finalize != 0: O = o / l -> o_out (bf16), lse = m + ln l -> lse_out;
+ *                  rows with l <= 0 set *degenerate_flag (device int) to 1.
+ *
+ * m is kept in natural-log units of scale*q.k like the reference; the
+ * kernel's lazy rescaling may leave m below the row maximum, which is a
+ * valid accumulator representation (o/l and m + ln l are invariant).
+ * GQA: q head h reads kv head h / (h_q / h_kv).
+ * ------------------------------------------------------------------------ */
+typedef struct da_fwd_args {
+  const void* q; /* bf16 [h_q, rows_q, d]  */
+  const void* k; /* bf16 [h_kv, rows_kv, d] */
+  const void* v; /* bf16 [h_kv, rows_kv, d] */
+  int64_t h_q, h_kv, rows_q, rows_kv, d;
+  const float* o_in; /* fp32 [h_q, rows_q, d] or NULL */
+  const float* m_in; /* fp32 [h_q, rows_q] */
+  const float* l_in;
+  float* o_acc; /* finalize == 0 */
+  float* m_acc;
+  float* l_acc;
+  void* o_out;    /* bf16, finalize != 0 */
+  float* lse_out; /* fp32 [h_q, rows_q] */
+  int* degenerate_flag; /* optional device int */
+  float scale;          /* <= 0 selects 1/sqrt(d) (runtime.cpp:150) */
+  int mask;             /* da_mask_mode */
+  int finalize;
+} da_fwd_args;
+
+da_status da_attn_fwd_chunk(const da_fwd_args* args, void* stream);
+
+/* rescale (flashcore.hpp:202-224): (o,m,l)_out = a ⊕ b over [h, rows]. Out may alias a. */
+da_status da_attn_merge(const float* o_a, const float* m_a, const float* l_a, const float* o_b,
+                        const float* m_b, const float* l_b, float* o_out, float* m_out,
+                        float* l_out, int64_t h, int64_t rows, int64_t d, void* stream);
+
+/* finalize (flashcore.hpp:227-240): O = o/l (bf16), lse = m + ln l; degenerate rows flagged. */
+da_status da_attn_finalize(const float* o, const float* m, const float* l, void* o_out,
+                           float* lse_out, int* degenerate_flag, int64_t h, int64_t rows,
+                           int64_t d, void* stream);
+
+/* Reads back a device degenerate flag (synchronises the stream): DA_OK or
+ * DA_ERR_DEGENERATE_ROW, the reference's DegenerateRowError. */
+da_status da_check_degenerate(const int* degenerate_flag, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Backward.
+ *
+ * da_attn_bwd_preprocess replaces backward_aux (flashcore.hpp:250-261):
+ *   D = rowsum(dO ∘ O) computed once per query chunk (the reference
+ *   recomputes it inside every block_attn_backward call, :294).
+ *
+ * da_attn_bwd_chunk replaces block_attn_backward (flashcore.hpp:269-337):
+ *   P = exp(scale q kᵀ − lse), dv += Pᵀ dO, dS = P ∘ (dO vᵀ − D),
+ *   dq += scale dS k, dk += scale dSᵀ q.
+ *   dq_acc is fp32 [h_q, rows_q, d] and is always accumulated into
+ *   (the reference's `s.dq += g.dq`, runtime.cpp:620,633).
+ *   dk_acc / dv_acc are fp32 [h_kv, rows_kv, d]; accumulate_kv != 0 adds,
+ *   otherwise overwrites (the reference returns the contribution, :290-291).
+ *   lse is the GLOBAL logsumexp of the query rows (flashcore.hpp:263-266).
+ * ------------------------------------------------------------------------ */
+da_status da_attn_bwd_preprocess(const void* d_out, const void* out, float* d_vec, int64_t h,
+                                 int64_t rows, int64_t d, void* stream);
+
+typedef struct da_bwd_args {
+  const void* q;     /* bf16 [h_q, rows_q, d] */
+  const void* k;     /* bf16 [h_kv, rows_kv, d] */
+  const void* v;     /* bf16 [h_kv, rows_kv, d] */
+  const void* d_out; /* bf16 [h_q, rows_q, d] */
+  const float* lse;  /* fp32 [h_q, rows_q] */
+  const float* d_vec; /* fp32 [h_q, rows_q] from da_attn_bwd_preprocess */
+  int64_t h_q, h_kv, rows_q, rows_kv, d;
+  float* dq_acc; /* fp32 [h_q, rows_q, d], += */
+  float* dk_acc; /* fp32 [h_kv, rows_kv, d] */
+  float* dv_acc;
+  int accumulate_kv;
+  float scale;
+  int mask;
+} da_bwd_args;
+
+da_status da_attn_bwd_chunk(const da_bwd_args* args, void* stream);
+
+/* fp32 -> bf16 conversion of gradient accumulators (dq/dk/dv outputs). */
+da_status da_convert_f32_bf16(const float* src, void* dst, int64_t n, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Schedules (schedule.hpp:21-119, schedule.cpp:60-108).
+ *
+ * Flat, field-exact encoding of Schedule:
+ *   tasks[i] = {step, kind, worker, query_owner, kv_owner, helper} (int32 x 6)
+ *     kind: 0 LocalAttn, 1 RemoteAttn, 2 RescaleMerge, 3 Idle (TaskKind order)
+ *     tasks appear step by step, P primaries ascending by worker then merges;
+ *   messages[i] = {step, from, to, kind} (int32 x 4)
+ *     kind: 0 KV, 1 Q, 2 PartialResult, 3 GradKV (PayloadKind order).
+ * Call once with NULL buffers to size them (counts are always written).
+ * ------------------------------------------------------------------------ */
+typedef enum da_schedule_kind { DA_SCHEDULE_RING = 0, DA_SCHEDULE_BALANCED = 1 } da_schedule_kind;
+
+da_status da_schedule_build(int workers, int kind, int32_t* steps_out, int32_t* tasks,
+                            int64_t* n_tasks, int32_t* messages, int64_t* n_messages);
+
+/* validate (schedule.cpp:121-258): returns the violation count; writes the
+ * first message into da_last_error() when nonzero. Negative on bad input. */
+int64_t da_schedule_validate(int workers, int32_t steps, const int32_t* tasks, int64_t n_tasks,
+                             const int32_t* messages, int64_t n_messages);
+
+/* ------------------------------------------------------------------------
+ * Runtime (runtime.cpp:491-529, 720-750), P logical workers on ONE device —
+ * the reference's stepper executor with device kernels: per step, every
+ * worker's action runs in schedule order; "messages" are device buffers.
+ * Shards are arrays of P device pointers, each [h, rows, d] (rows = N/P).
+ * ------------------------------------------------------------------------ */
+typedef struct da_shards {
+  int32_t workers;
+  int64_t h_q, h_kv, rows, d;
+  const void* const* q; /* P pointers, bf16 */
+  const void* const* k;
+  const void* const* v;
+  void* const* out;     /* bf16 O, written by forward  (SequenceShard.out) */
+  float* const* lse;    /* fp32, written by forward    (SequenceShard.lse) */
+  const void* const* d_out; /* bf16, read by backward (SequenceShard.d_out) */
+  float* const* dq;     /* fp32, written by backward */
+  float* const* dk;
+  float* const* dv;
+} da_shards;
+
+typedef struct da_counters {
+  /* CommCounters, runtime.hpp:49-63 (scalars per payload kind), plus bytes */
+  int64_t kv_scalars, q_scalars, partial_scalars, grad_scalars;
+  int64_t kv_messages, q_messages, partial_messages, grad_messages;
+  int64_t attention_kernel_calls;
+  int32_t max_remote_chunks_held;
+} da_counters;
+
+/* schedule_kind: da_schedule_kind. workspace is allocated internally on the
+ * first call and cached per thread (not on the timed hot path). */
+da_status da_run_forward(const da_shards* shards, int schedule_kind, da_counters* counters,
+                         void* stream);
+da_status da_run_backward(const da_shards* shards, da_counters* counters, void* stream);
+/* Frees the cached runtime workspace of the calling thread. */
+void da_runtime_release(void);
+
+/* Debug: compute the raw score block S = q kᵀ (fp32, unscaled) of the first
+ * 128x128 tile of head 0 through the forward kernel's MMA path. */
+da_status da_debug_scores(const void* q, const void* k, int64_t rows, float* s_out, void* stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DISTATTN_B200_H */

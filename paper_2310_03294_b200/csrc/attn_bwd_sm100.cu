@@ -1,0 +1,440 @@
+// Chunk-attention backward for sm_100a: the gradient contributions of one
+// (query chunk, kv chunk) pair, rebuilt from the saved global logsumexp.
+//
+// Reference semantics: block_attn_backward (flashcore.hpp:269-337)
+//   P = exp(scale q k^T - lse); dV += P^T dO; dS = P o (dO v^T - D);
+//   dQ += scale dS k;  dK += scale dS^T q;   D = rowsum(dO o O) precomputed.
+//
+// Design (per CTA = one kv head x one 128-row kv tile; loops over every
+// (query head of the GQA group, query tile) that sees the kv tile):
+//   warp 0-3   dQ drain: tcgen05.ld of dQ^T, coalesced fp32 red.add into dq_acc
+//   warp 4-11  compute: P, dS for (kv row = TMEM lane, 64 query columns each)
+//   warp 12    MMA issuer (one thread)
+//   warp 13    loader: TMA for K/V (once), Q (2 stages), dO (1 stage); lse/D rows
+// TMEM (512 cols): dV [0,128) dK [128,256) S|P [256,384) dP|dS|dQ^T [384,512)
+//   S^T  = K Q^T          (SS, M=kv,  N=q)  -> S region
+//   dP^T = V dO^T         (SS, M=kv,  N=q)  -> dP region
+//   dV  += P^T dO         (TS, A = P^T in TMEM, B = dO MN-major)
+//   dK  += dS^T Q         (TS, A = dS^T in TMEM, B = Q MN-major)
+//   dQ^T = K^T dS^T       (SS, A = K MN-major, B = dS^T smem MN-major) -> dP region
+// Computing dQ transposed puts the head dim on TMEM lanes, so the drain warp
+// writes 32 consecutive floats of one dQ row per instruction (128 B).
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "kernels.h"
+#include "sm100_ptx.cuh"
+
+namespace da {
+namespace bwd {
+
+constexpr int kBM = 128;  // query rows per iteration
+constexpr int kBN = 128;  // kv rows per CTA
+constexpr int kHD = 128;
+constexpr uint32_t kTileBytes = 128 * 128 * 2;
+constexpr uint32_t kHalfTile = kTileBytes / 2;
+constexpr int kThreads = 448;
+constexpr uint32_t kColS = 256;
+constexpr uint32_t kColDP = 384;
+
+struct SmemLayout {
+  static constexpr uint32_t k = 0;
+  static constexpr uint32_t v = k + kTileBytes;
+  static constexpr uint32_t q = v + kTileBytes;        // 2 stages
+  static constexpr uint32_t dout = q + 2 * kTileBytes;  // 1 stage
+  static constexpr uint32_t ds = dout + kTileBytes;     // dS^T [kv][q] bf16, SW128 MN-major
+  static constexpr uint32_t vecs = ds + kTileBytes;     // 2 stages x (lse2[128], D[128])
+  static constexpr uint32_t bars = vecs + 2 * 2 * 128 * 4;
+  static constexpr uint32_t total = bars + 256;
+};
+constexpr size_t kSmemBytes = SmemLayout::total + 1024;
+
+struct Bars {
+  uint64_t kv_full;
+  uint64_t q_full[2];
+  uint64_t q_empty[2];
+  uint64_t do_full;
+  uint64_t do_empty;
+  uint64_t s_full;
+  uint64_t dp_full;
+  uint64_t p_full;
+  uint64_t ds_full;
+  uint64_t dq_full;
+  uint64_t dq_drained;
+  uint64_t acc_full;
+  uint32_t tmem_base;
+};
+static_assert(sizeof(Bars) <= 256, "barrier block");
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                    const __grid_constant__ CUtensorMap tmap_k,
+                    const __grid_constant__ CUtensorMap tmap_v,
+                    const __grid_constant__ CUtensorMap tmap_do, const BwdParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Bars* bars = reinterpret_cast<Bars*>(smem + SmemLayout::bars);
+  float* vecs = reinterpret_cast<float*>(smem + SmemLayout::vecs);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = threadIdx.x & 31;
+
+  // ---- work: kv tiles with the most query tiles first (causal)
+  const int n_q_tiles = (p.rows_q + kBM - 1) / kBM;
+  const int n_kv_tiles = (p.rows_kv + kBN - 1) / kBN;
+  const int kv_head = blockIdx.x % p.h_kv;
+  const int jt = static_cast<int>(blockIdx.x / p.h_kv);  // ascending: diag-heavy first
+  const int group = p.h_q / p.h_kv;
+  const int i0 = (p.mask == DA_MASK_DIAGONAL) ? jt : 0;
+  const int n_i = n_q_tiles - i0;
+  const int n_it = n_i > 0 ? group * n_i : 0;
+  (void)n_kv_tiles;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_init(&bars->kv_full, 1);
+      for (int s = 0; s < 2; ++s) {
+        mbar_init(&bars->q_full[s], 1);
+        mbar_init(&bars->q_empty[s], 1);
+      }
+      mbar_init(&bars->do_full, 1);
+      mbar_init(&bars->do_empty, 1);
+      mbar_init(&bars->s_full, 1);
+      mbar_init(&bars->dp_full, 1);
+      mbar_init(&bars->p_full, 256);
+      mbar_init(&bars->ds_full, 256);
+      mbar_init(&bars->dq_full, 1);
+      mbar_init(&bars->dq_drained, 128);
+      mbar_init(&bars->acc_full, 1);
+      fence_barrier_init();
+    }
+  } else if (warp == 13) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tmap_q);
+      tma_prefetch_desc(&tmap_k);
+      tma_prefetch_desc(&tmap_v);
+      tma_prefetch_desc(&tmap_do);
+    }
+  } else if (warp == 12) {
+    tmem_alloc<512>(&bars->tmem_base);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  auto it_head = [&](int it) { return kv_head * group + it / n_i; };
+  auto it_qtile = [&](int it) { return i0 + it % n_i; };
+
+  if (warp == 13) {
+    // ===================== loader =====================
+    constexpr float kLog2e = 1.4426950408889634f;
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&bars->kv_full, 2 * kTileBytes);
+      tma_load_3d(smem + SmemLayout::k, &tmap_k, &bars->kv_full, 0, jt * kBN, kv_head);
+      tma_load_3d(smem + SmemLayout::k + kHalfTile, &tmap_k, &bars->kv_full, 64, jt * kBN, kv_head);
+      tma_load_3d(smem + SmemLayout::v, &tmap_v, &bars->kv_full, 0, jt * kBN, kv_head);
+      tma_load_3d(smem + SmemLayout::v + kHalfTile, &tmap_v, &bars->kv_full, 64, jt * kBN, kv_head);
+    }
+    for (int it = 0; it < n_it; ++it) {
+      const int st = it & 1;
+      const uint32_t ph = (it >> 1) & 1;
+      const int hq = it_head(it);
+      const int row0 = it_qtile(it) * kBM;
+      mbar_wait(&bars->q_empty[st], ph ^ 1);
+      // lse (log2 units) and D for the 128 query rows; padding rows get
+      // lse2 = +inf so their probabilities are exactly zero.
+      float* lse2 = vecs + st * 256;
+      float* dvec = lse2 + 128;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int r = lane * 4 + k;
+        const int row = row0 + r;
+        float l2 = INFINITY, dd = 0.f;
+        if (row < p.rows_q) {
+          const size_t idx = static_cast<size_t>(hq) * p.rows_q + row;
+          l2 = p.lse[idx] * kLog2e;
+          dd = p.d_vec[idx];
+        }
+        lse2[r] = l2;
+        dvec[r] = dd;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&bars->q_full[st], kTileBytes);
+        uint8_t* qs = smem + SmemLayout::q + st * kTileBytes;
+        tma_load_3d(qs, &tmap_q, &bars->q_full[st], 0, row0, hq);
+        tma_load_3d(qs + kHalfTile, &tmap_q, &bars->q_full[st], 64, row0, hq);
+        mbar_wait(&bars->do_empty, (it & 1) ^ 1);
+        mbar_arrive_expect_tx(&bars->do_full, kTileBytes);
+        tma_load_3d(smem + SmemLayout::dout, &tmap_do, &bars->do_full, 0, row0, hq);
+        tma_load_3d(smem + SmemLayout::dout + kHalfTile, &tmap_do, &bars->do_full, 64, row0, hq);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 12) {
+    // ===================== MMA issuer =====================
+    if (lane == 0 && n_it > 0) {
+      constexpr uint32_t idesc_kk = make_idesc_bf16(128, 128, false, false);  // S, dP
+      constexpr uint32_t idesc_kmn = make_idesc_bf16(128, 128, false, true);  // dV, dK
+      constexpr uint32_t idesc_mnmn = make_idesc_bf16(128, 128, true, true);  // dQ^T
+      const uint32_t k_addr = smem_u32(smem + SmemLayout::k);
+      const uint32_t v_addr = smem_u32(smem + SmemLayout::v);
+      const uint32_t q_addr = smem_u32(smem + SmemLayout::q);
+      const uint32_t do_addr = smem_u32(smem + SmemLayout::dout);
+      const uint32_t ds_addr = smem_u32(smem + SmemLayout::ds);
+
+      // D = A B^T with both operands K-major [128][128] SW128 tiles
+      auto gemm_kk = [&](uint32_t d_tmem, uint32_t a, uint32_t b) {
+#pragma unroll
+        for (int kk = 0; kk < kHD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * kHalfTile + (kk & 3) * 32;
+          mma_ss(d_tmem, make_sdesc_sw128(a + off, 16, 1024), make_sdesc_sw128(b + off, 16, 1024),
+                 idesc_kk, kk > 0 ? 1u : 0u);
+        }
+      };
+      // D (+)= A[tmem, K = query columns split in two 64-col halves] * B (MN-major [q][d])
+      auto gemm_ts = [&](uint32_t d_tmem, uint32_t a_tmem, uint32_t b, bool acc) {
+#pragma unroll
+        for (int kk = 0; kk < kBM / 16; ++kk) {
+          const uint32_t a_col = a_tmem + (kk >> 2) * 64 + (kk & 3) * 8;
+          mma_ts(d_tmem, a_col, make_sdesc_sw128(b + kk * 2048, kHalfTile, 1024), idesc_kmn,
+                 (acc || kk > 0) ? 1u : 0u);
+        }
+      };
+
+      mbar_wait(&bars->kv_full, 0);
+      mbar_wait(&bars->q_full[0], 0);
+      tc_fence_after();
+      gemm_kk(tmem + kColS, k_addr, q_addr);
+      mma_commit(&bars->s_full);
+      mbar_wait(&bars->do_full, 0);
+      tc_fence_after();
+      gemm_kk(tmem + kColDP, v_addr, do_addr);
+      mma_commit(&bars->dp_full);
+
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it & 1;
+        const bool has_next = it + 1 < n_it;
+        // dV += P^T dO
+        mbar_wait(&bars->p_full, it & 1);
+        tc_fence_after();
+        gemm_ts(tmem + 0, tmem + kColS, do_addr, it > 0);
+        mma_commit(&bars->do_empty);
+        // next S^T (overwrites P only after dV has consumed it: in-order pipe)
+        if (has_next) {
+          const int st1 = (it + 1) & 1;
+          mbar_wait(&bars->q_full[st1], ((it + 1) >> 1) & 1);
+          tc_fence_after();
+          gemm_kk(tmem + kColS, k_addr, q_addr + st1 * kTileBytes);
+          mma_commit(&bars->s_full);
+        }
+        // dK += dS^T Q
+        mbar_wait(&bars->ds_full, it & 1);
+        tc_fence_after();
+        gemm_ts(tmem + 128, tmem + kColDP, q_addr + st * kTileBytes, it > 0);
+        mma_commit(&bars->q_empty[st]);
+        // dQ^T = K^T dS^T  (A = K MN-major, B = dS^T MN-major)
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk) {
+          mma_ss(tmem + kColDP, make_sdesc_sw128(k_addr + kk * 2048, kHalfTile, 1024),
+                 make_sdesc_sw128(ds_addr + kk * 2048, kHalfTile, 1024), idesc_mnmn,
+                 kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&bars->dq_full);
+        // next dP^T once dQ^T has left TMEM
+        if (has_next) {
+          mbar_wait(&bars->dq_drained, it & 1);
+          mbar_wait(&bars->do_full, (it + 1) & 1);
+          tc_fence_after();
+          gemm_kk(tmem + kColDP, v_addr, do_addr);
+          mma_commit(&bars->dp_full);
+        }
+      }
+      mma_commit(&bars->acc_full);
+    }
+  } else if (warp < 4) {
+    // ===================== dQ drain =====================
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    const int dcol = warp * 32 + lane;  // head-dim index = TMEM lane of dQ^T
+    for (int it = 0; it < n_it; ++it) {
+      const int hq = it_head(it);
+      const int row0 = it_qtile(it) * kBM;
+      mbar_wait(&bars->dq_full, it & 1);
+      tc_fence_after();
+      float* base = p.dq_acc + (static_cast<size_t>(hq) * p.rows_q + row0) * kHD + dcol;
+      const int q_valid = min(kBM, p.rows_q - row0);
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(lane_base + kColDP + c * 32, r);
+        tmem_ld_wait();
+        if (c == 3) {
+          tc_fence_before();
+          mbar_arrive(&bars->dq_drained);
+        }
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const int q = c * 32 + k;
+          if (q < q_valid) red_add_f32(base + static_cast<size_t>(q) * kHD, p.scale * __uint_as_float(r[k]));
+        }
+      }
+    }
+  } else {
+    // ===================== compute (warps 4-11) =====================
+    const int cw = warp - 4;
+    const int quarter = cw & 3;
+    const int half = cw >> 2;
+    const int r = quarter * 32 + lane;  // kv row within tile = TMEM lane
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+    const uint32_t s_tmem = lane_base + kColS + half * 64;
+    const uint32_t dp_tmem = lane_base + kColDP + half * 64;
+    const float sl2 = p.scale_log2;
+    uint8_t* ds_smem = smem + SmemLayout::ds + half * kHalfTile + r * 128;
+
+    for (int it = 0; it < n_it; ++it) {
+      const int st = it & 1;
+      const bool diag = (p.mask == DA_MASK_DIAGONAL) && (it_qtile(it) == jt);
+      const float* lse2 = vecs + st * 256 + half * 64;
+      const float* dvec = vecs + st * 256 + 128 + half * 64;
+      mbar_wait(&bars->q_full[st], (it >> 1) & 1);  // lse/D rows visible
+
+      // ---- phase A: P = exp2(S * scale*log2e - lse2)
+      mbar_wait(&bars->s_full, it & 1);
+      tc_fence_after();
+      uint32_t sr[2][32];
+      tmem_ld_32x32b_x32(s_tmem, sr[0]);
+      tmem_ld_32x32b_x32(s_tmem + 32, sr[1]);
+      tmem_ld_wait();
+      float pr[64];
+#pragma unroll
+      for (int c = 0; c < 64; c += 4) {
+        const float4 l4 = *reinterpret_cast<const float4*>(lse2 + c);
+        pr[c + 0] = ex2_approx(fmaf(__uint_as_float(sr[c >> 5][(c + 0) & 31]), sl2, -l4.x));
+        pr[c + 1] = ex2_approx(fmaf(__uint_as_float(sr[c >> 5][(c + 1) & 31]), sl2, -l4.y));
+        pr[c + 2] = ex2_approx(fmaf(__uint_as_float(sr[c >> 5][(c + 2) & 31]), sl2, -l4.z));
+        pr[c + 3] = ex2_approx(fmaf(__uint_as_float(sr[c >> 5][(c + 3) & 31]), sl2, -l4.w));
+      }
+      if (diag) {
+        // query column (half*64 + c) is visible from kv row r iff q >= r
+#pragma unroll
+        for (int c = 0; c < 64; ++c)
+          if (half * 64 + c < r) pr[c] = 0.f;
+      }
+      {
+        uint32_t pk[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) pk[c] = pack_bf16x2(pr[2 * c], pr[2 * c + 1]);
+        tmem_st_32x32b_x32(s_tmem, pk);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&bars->p_full);
+
+      // ---- phase B: dS = P o (dP - D)
+      mbar_wait(&bars->dp_full, it & 1);
+      tc_fence_after();
+      uint32_t dsk[32];
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t dr[32];
+        tmem_ld_32x32b_x32(dp_tmem + hh * 32, dr);
+        tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < 32; c += 4) {
+          const float4 d4 = *reinterpret_cast<const float4*>(dvec + hh * 32 + c);
+          const int b = hh * 32 + c;
+          const float s0 = pr[b + 0] * (__uint_as_float(dr[c + 0]) - d4.x);
+          const float s1 = pr[b + 1] * (__uint_as_float(dr[c + 1]) - d4.y);
+          const float s2 = pr[b + 2] * (__uint_as_float(dr[c + 2]) - d4.z);
+          const float s3 = pr[b + 3] * (__uint_as_float(dr[c + 3]) - d4.w);
+          dsk[(b >> 1) + 0] = pack_bf16x2(s0, s1);
+          dsk[(b >> 1) + 1] = pack_bf16x2(s2, s3);
+        }
+      }
+      // dS^T (bf16) -> TMEM (A operand of dK) and -> smem (B operand of dQ^T)
+      tmem_st_32x32b_x32(dp_tmem, dsk);
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        const int phys = ch ^ (r & 7);
+        *reinterpret_cast<uint4*>(ds_smem + phys * 16) =
+            make_uint4(dsk[4 * ch + 0], dsk[4 * ch + 1], dsk[4 * ch + 2], dsk[4 * ch + 3]);
+      }
+      fence_proxy_async_smem();
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&bars->ds_full);
+    }
+
+    // ===================== epilogue: dV, dK rows =====================
+    if (n_it > 0) {
+      mbar_wait(&bars->acc_full, 0);
+      tc_fence_after();
+      const int row = jt * kBN + r;
+      const bool valid = row < p.rows_kv;
+      const size_t base = (static_cast<size_t>(kv_head) * p.rows_kv + row) * kHD + half * 64;
+#pragma unroll 1
+      for (int which = 0; which < 2; ++which) {
+        float* dst = (which == 0 ? p.dv_acc : p.dk_acc) + base;
+        const float f = which == 0 ? 1.f : p.scale;
+#pragma unroll 1
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t a[32];
+          tmem_ld_32x32b_x32(lane_base + which * 128 + half * 64 + hh * 32, a);
+          tmem_ld_wait();
+          if (!valid) continue;
+          float4* d4 = reinterpret_cast<float4*>(dst + hh * 32);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            float4 x = make_float4(f * __uint_as_float(a[4 * i]), f * __uint_as_float(a[4 * i + 1]),
+                                   f * __uint_as_float(a[4 * i + 2]),
+                                   f * __uint_as_float(a[4 * i + 3]));
+            if (p.accumulate_kv) {
+              const float4 o = d4[i];
+              x.x += o.x;
+              x.y += o.y;
+              x.z += o.z;
+              x.w += o.w;
+            }
+            d4[i] = x;
+          }
+        }
+      }
+    } else if (p.mask != DA_MASK_EMPTY && !p.accumulate_kv) {
+      // no query tile sees this kv tile: contribution is zero
+      const int row = jt * kBN + r;
+      if (row < p.rows_kv) {
+        const size_t base = (static_cast<size_t>(kv_head) * p.rows_kv + row) * kHD + half * 64;
+        for (int i = 0; i < 64; i += 4) {
+          *reinterpret_cast<float4*>(p.dv_acc + base + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+          *reinterpret_cast<float4*>(p.dk_acc + base + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 12) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace bwd
+
+cudaError_t launch_attn_bwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                            const CUtensorMap& tdo, const BwdParams& p, cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(bwd::attn_bwd_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(bwd::kSmemBytes));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int n_kv_tiles = (p.rows_kv + bwd::kBN - 1) / bwd::kBN;
+  dim3 grid(n_kv_tiles * p.h_kv);
+  bwd::attn_bwd_kernel<<<grid, bwd::kThreads, bwd::kSmemBytes, stream>>>(tq, tk, tv, tdo, p);
+  return cudaGetLastError();
+}
+
+}  // namespace da

@@ -1,0 +1,414 @@
+// Chunk-attention forward for sm_100a: one (query chunk, kv chunk) online-
+// softmax update with the incoming-accumulator merge and finalize fused into
+// the epilogue.
+//
+// Reference semantics: block_attn_update (flashcore.hpp:135-197) followed by
+// rescale (flashcore.hpp:202-224) with the caller's accumulator and, on the
+// last step, finalize (flashcore.hpp:227-240).
+//
+// Design (per CTA = one head x two 128-row query tiles "pair"):
+//   warp 0-3  softmax for query tile 0  (thread = query row = TMEM lane)
+//   warp 4-7  softmax for query tile 1
+//   warp 8    MMA issuer (one thread): S_t = Q_t K_j^T (SS), O_t += P_t V_j (TS)
+//   warp 9    TMA producer: Q once, K_j / V_j through a 2-stage ring
+// TMEM (512 cols): S_0 [0,128) S_1 [128,256) O_0 [256,384) O_1 [384,512);
+// P_t (bf16) aliases the upper half of S_t. The two query tiles ping-pong:
+// while softmax t works on S_t(j) the tensor core runs the other tile's MMAs.
+// O is rescaled lazily (only when the running max grows by > 2^8).
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "kernels.h"
+#include "sm100_ptx.cuh"
+
+namespace da {
+namespace fwd {
+
+constexpr int kBM = 128;
+constexpr int kBN = 128;
+constexpr int kHD = 128;
+constexpr int kStages = 2;
+constexpr uint32_t kTileBytes = kBM * kHD * 2;  // 32 KB, one 128x128 bf16 tile
+constexpr uint32_t kHalfTile = kTileBytes / 2;  // one 64-column SW128 box
+constexpr int kThreads = 320;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+struct SmemLayout {
+  // all tiles 1024B aligned (SW128)
+  static constexpr uint32_t q0 = 0;
+  static constexpr uint32_t q1 = q0 + kTileBytes;
+  static constexpr uint32_t k = q1 + kTileBytes;                 // kStages tiles
+  static constexpr uint32_t v = k + kStages * kTileBytes;        // kStages tiles
+  static constexpr uint32_t bars = v + kStages * kTileBytes;     // barriers
+  static constexpr uint32_t total = bars + 256;
+};
+constexpr size_t kSmemBytes = SmemLayout::total + 1024;  // + alignment slack
+
+struct Bars {
+  uint64_t q_full;
+  uint64_t k_full[kStages];
+  uint64_t k_empty[kStages];
+  uint64_t v_full[kStages];
+  uint64_t v_empty[kStages];
+  uint64_t s_full[2];
+  uint64_t p_full[2];
+  uint64_t o_done[2];
+  uint32_t tmem_base;
+};
+static_assert(sizeof(Bars) <= 256, "barrier block");
+
+__device__ __forceinline__ int tiles_for(int mask, int qt, int n_kv_tiles) {
+  // Diagonal: query tile qt sees kv tiles 0..qt. Full: every kv tile.
+  return mask == DA_MASK_DIAGONAL ? min(qt + 1, n_kv_tiles) : n_kv_tiles;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                    const __grid_constant__ CUtensorMap tmap_k,
+                    const __grid_constant__ CUtensorMap tmap_v, const FwdParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Bars* bars = reinterpret_cast<Bars*>(smem + SmemLayout::bars);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = threadIdx.x & 31;
+
+  // ---- work assignment: heavy (late) query pairs first under causal masks
+  const int n_q_tiles = (p.rows_q + kBM - 1) / kBM;
+  const int n_kv_tiles = (p.rows_kv + kBN - 1) / kBN;
+  const int n_pairs = (n_q_tiles + 1) / 2;
+  const int head = blockIdx.x % p.h_q;
+  const int pair = n_pairs - 1 - static_cast<int>(blockIdx.x / p.h_q);
+  const int kv_head = head / (p.h_q / p.h_kv);
+  const int qt0 = 2 * pair;
+  const bool has_t1 = (qt0 + 1) < n_q_tiles;
+  const int n0 = tiles_for(p.mask, qt0, n_kv_tiles);
+  const int n1 = has_t1 ? tiles_for(p.mask, qt0 + 1, n_kv_tiles) : 0;
+  const int nmax = max(n0, n1);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_init(&bars->q_full, 1);
+      for (int s = 0; s < kStages; ++s) {
+        mbar_init(&bars->k_full[s], 1);
+        mbar_init(&bars->k_empty[s], 1);
+        mbar_init(&bars->v_full[s], 1);
+        mbar_init(&bars->v_empty[s], 1);
+      }
+      for (int t = 0; t < 2; ++t) {
+        mbar_init(&bars->s_full[t], 1);
+        mbar_init(&bars->p_full[t], 128);
+        mbar_init(&bars->o_done[t], 1);
+      }
+      fence_barrier_init();
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tmap_q);
+      tma_prefetch_desc(&tmap_k);
+      tma_prefetch_desc(&tmap_v);
+    }
+  } else if (warp == 8) {
+    tmem_alloc<512>(&bars->tmem_base);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  if (warp == 9) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      const int row0 = qt0 * kBM;
+      mbar_arrive_expect_tx(&bars->q_full, (has_t1 ? 2u : 1u) * kTileBytes);
+      tma_load_3d(smem + SmemLayout::q0, &tmap_q, &bars->q_full, 0, row0, head);
+      tma_load_3d(smem + SmemLayout::q0 + kHalfTile, &tmap_q, &bars->q_full, 64, row0, head);
+      if (has_t1) {
+        tma_load_3d(smem + SmemLayout::q1, &tmap_q, &bars->q_full, 0, row0 + kBM, head);
+        tma_load_3d(smem + SmemLayout::q1 + kHalfTile, &tmap_q, &bars->q_full, 64, row0 + kBM,
+                    head);
+      }
+      for (int j = 0; j < nmax; ++j) {
+        const int s = j % kStages;
+        const uint32_t ph = (j / kStages) & 1;
+        uint8_t* ks = smem + SmemLayout::k + s * kTileBytes;
+        uint8_t* vs = smem + SmemLayout::v + s * kTileBytes;
+        mbar_wait(&bars->k_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&bars->k_full[s], kTileBytes);
+        tma_load_3d(ks, &tmap_k, &bars->k_full[s], 0, j * kBN, kv_head);
+        tma_load_3d(ks + kHalfTile, &tmap_k, &bars->k_full[s], 64, j * kBN, kv_head);
+        mbar_wait(&bars->v_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&bars->v_full[s], kTileBytes);
+        tma_load_3d(vs, &tmap_v, &bars->v_full[s], 0, j * kBN, kv_head);
+        tma_load_3d(vs + kHalfTile, &tmap_v, &bars->v_full[s], 64, j * kBN, kv_head);
+      }
+    }
+  } else if (warp == 8) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      constexpr uint32_t idesc_qk = make_idesc_bf16(128, 128, false, false);
+      constexpr uint32_t idesc_pv = make_idesc_bf16(128, 128, false, true);
+      const uint32_t q_addr[2] = {smem_u32(smem + SmemLayout::q0), smem_u32(smem + SmemLayout::q1)};
+      const uint32_t k_addr = smem_u32(smem + SmemLayout::k);
+      const uint32_t v_addr = smem_u32(smem + SmemLayout::v);
+      const int n_t[2] = {n0, n1};
+
+      auto issue_s = [&](int t, int stage) {
+        const uint32_t kb = k_addr + stage * kTileBytes;
+        const uint32_t d_tmem = tmem + t * 128;
+#pragma unroll
+        for (int kk = 0; kk < kHD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * kHalfTile + (kk & 3) * 32;
+          const uint64_t a = make_sdesc_sw128(q_addr[t] + off, 16, 1024);
+          const uint64_t b = make_sdesc_sw128(kb + off, 16, 1024);
+          mma_ss(d_tmem, a, b, idesc_qk, kk > 0 ? 1u : 0u);
+        }
+      };
+      auto issue_pv = [&](int t, int stage, bool acc) {
+        const uint32_t vb = v_addr + stage * kTileBytes;
+        const uint32_t d_tmem = tmem + 256 + t * 128;
+        const uint32_t p_tmem = tmem + t * 128 + 64;
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk) {
+          const uint64_t b = make_sdesc_sw128(vb + kk * 2048, kHalfTile, 1024);
+          mma_ts(d_tmem, p_tmem + kk * 8, b, idesc_pv, (acc || kk > 0) ? 1u : 0u);
+        }
+      };
+
+      mbar_wait(&bars->q_full, 0);
+      if (nmax > 0) {
+        mbar_wait(&bars->k_full[0], 0);
+        tc_fence_after();
+        for (int t = 0; t < 2; ++t) {
+          if (n_t[t] > 0) {
+            issue_s(t, 0);
+            mma_commit(&bars->s_full[t]);
+          }
+        }
+        mma_commit(&bars->k_empty[0]);
+      }
+      for (int j = 0; j < nmax; ++j) {
+        const int s = j % kStages;
+        const uint32_t ph = (j / kStages) & 1;
+        const bool has_next = j + 1 < nmax;
+        const int s1 = (j + 1) % kStages;
+        const uint32_t ph1 = ((j + 1) / kStages) & 1;
+        mbar_wait(&bars->v_full[s], ph);
+        if (has_next) mbar_wait(&bars->k_full[s1], ph1);
+        tc_fence_after();
+        for (int t = 0; t < 2; ++t) {
+          if (j < n_t[t]) {
+            mbar_wait(&bars->p_full[t], j & 1);
+            tc_fence_after();
+            issue_pv(t, s, j > 0);
+            mma_commit(&bars->o_done[t]);
+            if (j + 1 < n_t[t]) {
+              issue_s(t, s1);
+              mma_commit(&bars->s_full[t]);
+            }
+          }
+        }
+        mma_commit(&bars->v_empty[s]);
+        if (has_next) mma_commit(&bars->k_empty[s1]);
+      }
+    }
+  } else {
+    // ===================== softmax / epilogue (warps 0-7) =====================
+    const int t = warp / 4;
+    const int quarter = warp % 4;
+    const int row_in_tile = quarter * 32 + lane;
+    const int qt = qt0 + t;
+    const int n_tiles = t == 0 ? n0 : n1;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+    const uint32_t s_tmem = lane_base + t * 128;
+    const uint32_t p_tmem = s_tmem + 64;
+    const uint32_t o_tmem = lane_base + 256 + t * 128;
+    const float sl2 = p.scale_log2;
+    const float neg_inf = -INFINITY;
+
+    float m_run = neg_inf;  // running max, log2 units of scale*q.k
+    float l_run = 0.f;
+
+    for (int j = 0; j < n_tiles; ++j) {
+      mbar_wait(&bars->s_full[t], j & 1);
+      tc_fence_after();
+      uint32_t sr[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(s_tmem + c * 32, sr[c]);
+      tmem_ld_wait();
+
+      if (p.debug_s != nullptr && j == 0 && t == 0 && blockIdx.x == 0) {
+        // raw (unscaled, unmasked) scores of the first tile, for layout tests
+        float* dst = p.debug_s + static_cast<size_t>(row_in_tile) * kBN;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) dst[c * 32 + i] = __uint_as_float(sr[c][i]);
+      }
+
+      // masking: causal inside the diagonal tile, ragged kv tail
+      const bool diag = (p.mask == DA_MASK_DIAGONAL) && (j == qt);
+      const int kv_valid = p.rows_kv - j * kBN;  // columns >= kv_valid are padding
+      float mx = neg_inf;
+      if (diag || kv_valid < kBN) {
+        const int lim = diag ? min(row_in_tile + 1, kv_valid) : kv_valid;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            if (c * 32 + i >= lim) sr[c][i] = __float_as_uint(neg_inf);
+            mx = fmaxf(mx, __uint_as_float(sr[c][i]));
+          }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(sr[c][i]));
+      }
+      mx *= sl2;
+
+      float alpha = 1.f;
+      const float m_new = fmaxf(m_run, mx);
+      const bool need = m_new > m_run + kRescaleThreshold;
+      if (need) {
+        alpha = (m_run == neg_inf) ? 0.f : ex2_approx(m_run - m_new);
+        m_run = m_new;
+      }
+      const float neg_m = (m_run == neg_inf) ? 0.f : -m_run;
+
+      float rs = 0.f;
+      uint32_t pk[2][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const float p0 = ex2_approx(fmaf(__uint_as_float(sr[c][i]), sl2, neg_m));
+          const float p1 = ex2_approx(fmaf(__uint_as_float(sr[c][i + 1]), sl2, neg_m));
+          rs += p0 + p1;
+          pk[c >> 1][(c & 1) * 16 + i / 2] = pack_bf16x2(p0, p1);
+        }
+      l_run = l_run * alpha + rs;
+
+      // lazy O correction: only warps with a row whose max jumped
+      if (j > 0 && __any_sync(0xffffffffu, need)) {
+        mbar_wait(&bars->o_done[t], (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t orr[32];
+          tmem_ld_32x32b_x32(o_tmem + c * 32, orr);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) orr[i] = __float_as_uint(__uint_as_float(orr[i]) * alpha);
+          tmem_st_32x32b_x32(o_tmem + c * 32, orr);
+        }
+      }
+      tmem_st_32x32b_x32(p_tmem, pk[0]);
+      tmem_st_32x32b_x32(p_tmem + 32, pk[1]);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&bars->p_full[t]);
+    }
+
+    // ===================== epilogue =====================
+    if (n_tiles > 0) {
+      mbar_wait(&bars->o_done[t], (n_tiles - 1) & 1);
+      tc_fence_after();
+      const int row = qt * kBM + row_in_tile;
+      const bool valid = row < p.rows_q;
+      const size_t srow = static_cast<size_t>(head) * p.rows_q + row;
+      constexpr float kLn2 = 0.69314718055994530942f;
+      const float m_k = m_run * kLn2;  // natural-log units
+      float wa = 0.f, wb = 1.f, m_out = m_k, l_out = l_run;
+      if (valid && p.o_in != nullptr) {
+        const float m_i = p.m_in[srow];
+        const float l_i = p.l_in[srow];
+        m_out = fmaxf(m_i, m_k);
+        wa = (m_i == neg_inf) ? 0.f : __expf(m_i - m_out);
+        wb = (m_k == neg_inf) ? 0.f : __expf(m_k - m_out);
+        l_out = wa * l_i + wb * l_run;
+      }
+      float inv_l = 0.f;
+      if (p.finalize && valid) {
+        if (!(l_out > 0.f)) {
+          if (p.degenerate_flag) atomicExch(p.degenerate_flag, 1);
+        } else {
+          inv_l = 1.f / l_out;
+        }
+      }
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t orr[32];
+        tmem_ld_32x32b_x32(o_tmem + c * 32, orr);
+        tmem_ld_wait();
+        if (!valid) continue;
+        float o[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(orr[i]) * wb;
+        if (p.o_in != nullptr) {
+          const float4* src = reinterpret_cast<const float4*>(p.o_in + srow * kHD + c * 32);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 x = src[i];
+            o[4 * i + 0] = fmaf(wa, x.x, o[4 * i + 0]);
+            o[4 * i + 1] = fmaf(wa, x.y, o[4 * i + 1]);
+            o[4 * i + 2] = fmaf(wa, x.z, o[4 * i + 2]);
+            o[4 * i + 3] = fmaf(wa, x.w, o[4 * i + 3]);
+          }
+        }
+        if (p.finalize) {
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.o_out) +
+                                                srow * kHD + c * 32);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            uint4 w;
+            w.x = pack_bf16x2(o[8 * i + 0] * inv_l, o[8 * i + 1] * inv_l);
+            w.y = pack_bf16x2(o[8 * i + 2] * inv_l, o[8 * i + 3] * inv_l);
+            w.z = pack_bf16x2(o[8 * i + 4] * inv_l, o[8 * i + 5] * inv_l);
+            w.w = pack_bf16x2(o[8 * i + 6] * inv_l, o[8 * i + 7] * inv_l);
+            dst[i] = w;
+          }
+        } else {
+          float4* dst = reinterpret_cast<float4*>(p.o_acc + srow * kHD + c * 32);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            dst[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+        }
+      }
+      if (valid) {
+        if (p.finalize) {
+          p.lse_out[srow] = (l_out > 0.f) ? m_out + __logf(l_out) : neg_inf;
+        } else {
+          p.m_acc[srow] = m_out;
+          p.l_acc[srow] = l_out;
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace fwd
+
+cudaError_t launch_attn_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                            const FwdParams& p, cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(fwd::attn_fwd_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(fwd::kSmemBytes));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int n_q_tiles = (p.rows_q + fwd::kBM - 1) / fwd::kBM;
+  const int n_pairs = (n_q_tiles + 1) / 2;
+  dim3 grid(n_pairs * p.h_q);
+  fwd::attn_fwd_kernel<<<grid, fwd::kThreads, fwd::kSmemBytes, stream>>>(tq, tk, tv, p);
+  return cudaGetLastError();
+}
+
+}  // namespace da

@@ -1,0 +1,17 @@
+// Shared host helpers of the C ABI implementation.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "../../include/distattn_b200.h"
+
+namespace da {
+da_status set_error(da_status s, const std::string& msg);
+da_status cuda_error(cudaError_t e, const char* where);
+const char* last_error();
+da_status make_tmap_3d(CUtensorMap* map, const void* base, int64_t heads, int64_t rows);
+cudaError_t launch_fill(float* dst, float value, int64_t n, cudaStream_t stream);
+}  // namespace da

@@ -1,0 +1,63 @@
+// Internal kernel parameter blocks and launchers (not part of the C ABI).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "../../include/distattn_b200.h"
+
+namespace da {
+
+struct FwdParams {
+  int h_q, h_kv, rows_q, rows_kv;
+  int mask;        // da_mask_mode (DIAGONAL or FULL; EMPTY never launches)
+  int finalize;
+  float scale_log2;  // scale * log2(e)
+  const float* o_in;
+  const float* m_in;
+  const float* l_in;
+  float* o_acc;
+  float* m_acc;
+  float* l_acc;
+  void* o_out;
+  float* lse_out;
+  int* degenerate_flag;
+  float* debug_s;  // optional raw-score dump of tile (0,0) of head 0
+};
+
+struct BwdParams {
+  int h_q, h_kv, rows_q, rows_kv;
+  int mask;
+  int accumulate_kv;
+  float scale;       // softmax scale (dq/dk factor)
+  float scale_log2;  // scale * log2(e)
+  const float* lse;    // [h_q, rows_q] natural log
+  const float* d_vec;  // [h_q, rows_q]
+  float* dq_acc;
+  float* dk_acc;
+  float* dv_acc;
+};
+
+cudaError_t launch_attn_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                            const FwdParams& p, cudaStream_t stream);
+
+cudaError_t launch_attn_bwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                            const CUtensorMap& tdo, const BwdParams& p, cudaStream_t stream);
+
+cudaError_t launch_merge(const float* o_a, const float* m_a, const float* l_a, const float* o_b,
+                         const float* m_b, const float* l_b, float* o_out, float* m_out,
+                         float* l_out, int64_t rows_total, cudaStream_t stream);
+
+cudaError_t launch_finalize(const float* o, const float* m, const float* l, void* o_out,
+                            float* lse_out, int* flag, int64_t rows_total, cudaStream_t stream);
+
+cudaError_t launch_bwd_preprocess(const void* d_out, const void* out, float* d_vec,
+                                  int64_t rows_total, cudaStream_t stream);
+
+cudaError_t launch_convert(const float* src, void* dst, int64_t n, cudaStream_t stream);
+
+cudaError_t launch_copy_acc(const float* o, const float* m, const float* l, float* o_out,
+                            float* m_out, float* l_out, int64_t rows_total, cudaStream_t stream);
+
+}  // namespace da

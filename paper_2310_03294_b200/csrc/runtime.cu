@@ -1,0 +1,309 @@
+// Device executor for P logical sequence-parallel workers on ONE GPU.
+//
+// This is the reference's stepper executor (runtime.cpp:266-330 forward,
+// :605-651 backward) with every per-chunk "kernel" a real sm_100a launch.
+// All shards live in one address space, so a message is the consumer
+// kernel reading the producer's buffer directly (zero-copy, the single-box
+// analogue of an NVSwitch peer read); counters still account each payload
+// exactly like count_message (runtime.cpp:50-83), scaled by the head count.
+//
+// Per-worker operation order is the reference's: at step t every worker's
+// primary task runs in ascending worker order, then the step's merges in
+// schedule order (helper-ascending) — runtime.cpp:286-328.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "capi_internal.h"
+#include "kernels.h"
+#include "schedule_impl.h"
+
+namespace da {
+namespace {
+
+struct Workspace {
+  int P = 0;
+  int64_t h_q = 0, rows = 0;
+  std::vector<float*> o, m, l;  // per worker running accumulator
+  std::vector<float*> po, pm, pl;  // per worker helper-partial slot
+  std::vector<float*> dvec;       // per worker D (backward)
+  int* flag = nullptr;
+  std::vector<void*> allocs;
+
+  void release() {
+    for (void* p : allocs) cudaFree(p);
+    allocs.clear();
+    o.clear(); m.clear(); l.clear(); po.clear(); pm.clear(); pl.clear(); dvec.clear();
+    flag = nullptr;
+    P = 0;
+  }
+  ~Workspace() { release(); }
+
+  cudaError_t ensure(int P_, int64_t h_q_, int64_t rows_) {
+    if (P_ == P && h_q_ == h_q && rows_ == rows) return cudaSuccess;
+    release();
+    const size_t acc = static_cast<size_t>(h_q_) * rows_;
+    auto get = [&](size_t bytes, void** out) {
+      cudaError_t e = cudaMalloc(out, bytes);
+      if (e == cudaSuccess) allocs.push_back(*out);
+      return e;
+    };
+    for (int w = 0; w < P_; ++w) {
+      void* buf = nullptr;
+      // o, m, l, po, pm, pl, dvec
+      cudaError_t e = get(acc * 4 * (2 * 128 + 5), &buf);
+      if (e != cudaSuccess) { release(); return e; }
+      float* f = static_cast<float*>(buf);
+      o.push_back(f); f += acc * 128;
+      po.push_back(f); f += acc * 128;
+      m.push_back(f); f += acc;
+      l.push_back(f); f += acc;
+      pm.push_back(f); f += acc;
+      pl.push_back(f); f += acc;
+      dvec.push_back(f);
+    }
+    void* fl = nullptr;
+    cudaError_t e = get(sizeof(int), &fl);
+    if (e != cudaSuccess) { release(); return e; }
+    flag = static_cast<int*>(fl);
+    P = P_;
+    h_q = h_q_;
+    rows = rows_;
+    return cudaSuccess;
+  }
+};
+
+thread_local Workspace g_ws;
+
+da_status check_shards(const da_shards* s, bool backward) {
+  if (s == nullptr) return set_error(DA_ERR_CONFIG, "null shards");
+  if (s->workers < 1) return set_error(DA_ERR_CONFIG, "need at least 1 worker");
+  if (s->d != 128) return set_error(DA_ERR_UNSUPPORTED, "d must be 128");
+  if (s->rows < 1) return set_error(DA_ERR_CONFIG, "tokens and d must be positive");
+  if (s->h_q < 1 || s->h_kv < 1 || s->h_q % s->h_kv != 0)
+    return set_error(DA_ERR_SHAPE, "h_q must be a positive multiple of h_kv");
+  for (int w = 0; w < s->workers; ++w) {
+    if (!s->q[w] || !s->k[w] || !s->v[w])
+      return set_error(DA_ERR_SHAPE, "all shards must share the same q/k/v shape");
+    if (backward) {
+      if (!s->out[w] || !s->lse[w])
+        return set_error(DA_ERR_STATE, "run_backward requires forward output and logsumexp");
+      if (!s->d_out[w]) return set_error(DA_ERR_STATE, "run_backward requires d_out on every shard");
+      if (!s->dq[w] || !s->dk[w] || !s->dv[w])
+        return set_error(DA_ERR_CONFIG, "run_backward: missing gradient buffers");
+    } else if (!s->out[w] || !s->lse[w]) {
+      return set_error(DA_ERR_CONFIG, "run_forward: missing output buffers");
+    }
+  }
+  return DA_OK;
+}
+
+struct Tally {
+  da_counters c{};
+  int held = 0, max_held = 0;
+  void acquire() { ++held; max_held = held > max_held ? held : max_held; }
+  void release() { --held; }
+};
+
+void count(da_counters& c, int kind, int64_t rows, int64_t d, int64_t heads) {
+  switch (kind) {
+    case kMsgKV: c.kv_scalars += 2 * rows * d * heads; ++c.kv_messages; break;
+    case kMsgQ: c.q_scalars += rows * d * heads; ++c.q_messages; break;
+    case kMsgPartial: c.partial_scalars += rows * (d + 2) * heads; ++c.partial_messages; break;
+    case kMsgGradKV: c.grad_scalars += 2 * rows * d * heads; ++c.grad_messages; break;
+  }
+}
+
+da_status fwd_update(const da_shards* s, int qw, int kvw, float* o_in, float* m_in, float* l_in,
+                     float* o, float* m, float* l, int mask, cudaStream_t st) {
+  da_fwd_args a{};
+  a.q = s->q[qw - 1];
+  a.k = s->k[kvw - 1];
+  a.v = s->v[kvw - 1];
+  a.h_q = s->h_q;
+  a.h_kv = s->h_kv;
+  a.rows_q = s->rows;
+  a.rows_kv = s->rows;
+  a.d = s->d;
+  a.o_in = o_in;
+  a.m_in = m_in;
+  a.l_in = l_in;
+  a.o_acc = o;
+  a.m_acc = m;
+  a.l_acc = l;
+  a.scale = 0.f;
+  a.mask = mask;
+  a.finalize = 0;
+  return da_attn_fwd_chunk(&a, st);
+}
+
+}  // namespace
+}  // namespace da
+
+using namespace da;
+
+extern "C" {
+
+void da_runtime_release(void) { g_ws.release(); }
+
+da_status da_run_forward(const da_shards* s, int schedule_kind, da_counters* counters,
+                         void* stream) {
+  da_status rc = check_shards(s, false);
+  if (rc != DA_OK) return rc;
+  const int P = s->workers;
+  if (schedule_kind != DA_SCHEDULE_RING && schedule_kind != DA_SCHEDULE_BALANCED)
+    return set_error(DA_ERR_CONFIG, "unknown schedule kind");
+  const FlatSchedule sch = schedule_kind == DA_SCHEDULE_RING ? make_ring(P) : make_balanced(P);
+  const auto errs = validate_flat(sch);
+  if (!errs.empty())
+    return set_error(DA_ERR_SCHEDULE, "invalid schedule: " + errs.front() + " (" +
+                                          std::to_string(errs.size()) + " violations)");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = g_ws.ensure(P, s->h_q, s->rows);
+  if (e != cudaSuccess) return cuda_error(e, "run_forward workspace");
+
+  std::vector<Tally> tally(P);
+  std::vector<bool> started(P, false);  // accumulator holds data (else fresh)
+  for (int t = 0; t < sch.steps; ++t) {
+    for (const Task& k : sch.tasks) {
+      if (k.step != t || k.kind == kIdle || k.kind == kMerge) continue;
+      const int w = k.worker;
+      Tally& me = tally[w - 1];
+      ++me.c.attention_kernel_calls;
+      float* o = g_ws.o[w - 1];
+      float* m = g_ws.m[w - 1];
+      float* l = g_ws.l[w - 1];
+      if (k.kind == kLocal) {
+        rc = fwd_update(s, w, w, started[w - 1] ? o : nullptr, m, l, o, m, l, DA_MASK_DIAGONAL, st);
+        started[w - 1] = true;
+      } else if (k.worker == k.query_owner) {  // Direct: kv chunk of kv_owner
+        me.acquire();
+        count(me.c, kMsgKV, s->rows, s->d, s->h_kv);
+        rc = fwd_update(s, w, k.kv_owner, started[w - 1] ? o : nullptr, m, l, o, m, l,
+                        DA_MASK_FULL, st);
+        started[w - 1] = true;
+        me.release();
+      } else {  // Help: owner's query against my kv, fresh partial
+        me.acquire();
+        count(me.c, kMsgQ, s->rows, s->d, s->h_q);
+        rc = fwd_update(s, k.query_owner, w, nullptr, nullptr, nullptr, g_ws.po[w - 1],
+                        g_ws.pm[w - 1], g_ws.pl[w - 1], DA_MASK_FULL, st);
+        me.release();
+      }
+      if (rc != DA_OK) return rc;
+    }
+    for (const Task& k : sch.tasks) {
+      if (k.step != t || k.kind != kMerge) continue;
+      const int ow = k.worker, hw = k.helper;
+      count(tally[ow - 1].c, kMsgPartial, s->rows, s->d, s->h_q);
+      e = launch_merge(g_ws.o[ow - 1], g_ws.m[ow - 1], g_ws.l[ow - 1], g_ws.po[hw - 1],
+                       g_ws.pm[hw - 1], g_ws.pl[hw - 1], g_ws.o[ow - 1], g_ws.m[ow - 1],
+                       g_ws.l[ow - 1], s->h_q * s->rows, st);
+      if (e != cudaSuccess) return cuda_error(e, "run_forward merge");
+    }
+  }
+  e = cudaMemsetAsync(g_ws.flag, 0, sizeof(int), st);
+  for (int w = 0; w < P && e == cudaSuccess; ++w)
+    e = launch_finalize(g_ws.o[w], g_ws.m[w], g_ws.l[w], s->out[w], s->lse[w], g_ws.flag,
+                        s->h_q * s->rows, st);
+  if (e != cudaSuccess) return cuda_error(e, "run_forward finalize");
+  if (counters) {
+    da_counters c{};
+    for (const Tally& ty : tally) {
+      c.kv_scalars += ty.c.kv_scalars; c.q_scalars += ty.c.q_scalars;
+      c.partial_scalars += ty.c.partial_scalars; c.grad_scalars += ty.c.grad_scalars;
+      c.kv_messages += ty.c.kv_messages; c.q_messages += ty.c.q_messages;
+      c.partial_messages += ty.c.partial_messages; c.grad_messages += ty.c.grad_messages;
+      c.attention_kernel_calls += ty.c.attention_kernel_calls;
+      c.max_remote_chunks_held = ty.max_held > c.max_remote_chunks_held ? ty.max_held
+                                                                         : c.max_remote_chunks_held;
+    }
+    *counters = c;
+  }
+  return da_check_degenerate(g_ws.flag, stream);
+}
+
+da_status da_run_backward(const da_shards* s, da_counters* counters, void* stream) {
+  da_status rc = check_shards(s, true);
+  if (rc != DA_OK) return rc;
+  const int P = s->workers;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = g_ws.ensure(P, s->h_q, s->rows);
+  if (e != cudaSuccess) return cuda_error(e, "run_backward workspace");
+  const int64_t q_elems = s->h_q * s->rows * 128;
+  const int64_t kv_elems = s->h_kv * s->rows * 128;
+  for (int w = 0; w < P; ++w) {
+    e = cudaMemsetAsync(s->dq[w], 0, q_elems * 4, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(s->dk[w], 0, kv_elems * 4, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(s->dv[w], 0, kv_elems * 4, st);
+    if (e == cudaSuccess)
+      e = launch_bwd_preprocess(s->d_out[w], s->out[w], g_ws.dvec[w], s->h_q * s->rows, st);
+    if (e != cudaSuccess) return cuda_error(e, "run_backward setup");
+  }
+  std::vector<Tally> tally(P);
+  auto chunk = [&](int qw, int kvw, int mask) {
+    da_bwd_args a{};
+    a.q = s->q[qw - 1];
+    a.k = s->k[kvw - 1];
+    a.v = s->v[kvw - 1];
+    a.d_out = s->d_out[qw - 1];
+    a.lse = s->lse[qw - 1];
+    a.d_vec = g_ws.dvec[qw - 1];
+    a.h_q = s->h_q;
+    a.h_kv = s->h_kv;
+    a.rows_q = s->rows;
+    a.rows_kv = s->rows;
+    a.d = s->d;
+    a.dq_acc = s->dq[qw - 1];
+    // GradKV: the contribution folds straight into the kv owner's buffers
+    a.dk_acc = s->dk[kvw - 1];
+    a.dv_acc = s->dv[kvw - 1];
+    a.accumulate_kv = 1;
+    a.scale = 0.f;
+    a.mask = mask;
+    return da_attn_bwd_chunk(&a, st);
+  };
+  // ring order (runtime.cpp:605-651): step 0 diagonal, then kv of p - t
+  for (int t = 0; t < P; ++t) {
+    for (int p = 1; p <= P; ++p) {
+      Tally& me = tally[p - 1];
+      if (t == 0) {
+        ++me.c.attention_kernel_calls;
+        rc = chunk(p, p, DA_MASK_DIAGONAL);
+      } else if (t < p) {
+        const int r = p - t;
+        count(me.c, kMsgKV, s->rows, s->d, s->h_kv);
+        me.acquire();
+        ++me.c.attention_kernel_calls;
+        rc = chunk(p, r, DA_MASK_FULL);
+        me.release();
+      }
+      if (rc != DA_OK) return rc;
+    }
+    if (t >= 1) {
+      for (int r = 1; r <= P; ++r) {
+        if (r + t > P) continue;
+        Tally& me = tally[r - 1];
+        count(me.c, kMsgGradKV, s->rows, s->d, s->h_kv);
+        me.acquire();
+        me.release();
+      }
+    }
+  }
+  if (counters) {
+    da_counters c{};
+    for (const Tally& ty : tally) {
+      c.kv_scalars += ty.c.kv_scalars; c.grad_scalars += ty.c.grad_scalars;
+      c.kv_messages += ty.c.kv_messages; c.grad_messages += ty.c.grad_messages;
+      c.attention_kernel_calls += ty.c.attention_kernel_calls;
+      c.max_remote_chunks_held = ty.max_held > c.max_remote_chunks_held ? ty.max_held
+                                                                         : c.max_remote_chunks_held;
+    }
+    *counters = c;
+  }
+  return DA_OK;
+}
+
+}  // extern "C"

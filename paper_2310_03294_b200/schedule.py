@@ -1,0 +1,189 @@
+"""Schedules, mirroring /root/reference/proj/include/distattn/schedule.hpp.
+
+The tables are built by the native library (csrc/schedule.cpp) and decoded
+here into the reference's Task / ScheduleMessage / Schedule shapes. Exact
+rational idle fractions and speedups use fractions.Fraction (rational.hpp).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import json
+from dataclasses import dataclass, field
+from fractions import Fraction
+
+from . import _lib
+from .errors import ConfigError, check
+
+
+class TaskKind(enum.IntEnum):
+    LocalAttn = 0
+    RemoteAttn = 1
+    RescaleMerge = 2
+    Idle = 3
+
+
+class PayloadKind(enum.IntEnum):
+    KV = 0
+    Q = 1
+    PartialResult = 2
+    GradKV = 3
+
+
+_TASK_NAMES = {0: "local_attn", 1: "remote_attn", 2: "rescale_merge", 3: "idle"}
+_PAYLOAD_NAMES = {0: "kv", 1: "q", 2: "partial", 3: "grad_kv"}
+
+
+@dataclass(frozen=True)
+class Task:
+    kind: TaskKind = TaskKind.Idle
+    worker: int = 0
+    query_owner: int = 0
+    kv_owner: int = 0
+    helper: int = 0
+
+    def is_attention(self) -> bool:
+        return self.kind in (TaskKind.LocalAttn, TaskKind.RemoteAttn)
+
+
+@dataclass(frozen=True)
+class ScheduleMessage:
+    step: int
+    from_: int
+    to: int
+    kind: PayloadKind
+
+
+@dataclass
+class Schedule:
+    workers: int = 0
+    steps: list = field(default_factory=list)      # list[list[Task]]
+    messages: list = field(default_factory=list)   # list[ScheduleMessage]
+
+    def step_count(self) -> int:
+        return len(self.steps)
+
+    def primaries(self, t: int):
+        return self.steps[t][: self.workers]
+
+    def merges(self, t: int):
+        return self.steps[t][self.workers:]
+
+    def attention_task_count(self) -> int:
+        return sum(1 for s in self.steps for t in s if t.is_attention())
+
+    def idle_slot_count(self) -> int:
+        return sum(1 for s in self.steps for t in s if t.kind == TaskKind.Idle)
+
+    def merge_count(self) -> int:
+        return sum(1 for s in self.steps for t in s if t.kind == TaskKind.RescaleMerge)
+
+    # flat encoding used by the C ABI
+    def flat(self):
+        tasks, msgs = [], []
+        for t, step in enumerate(self.steps):
+            for k in step:
+                tasks += [t, int(k.kind), k.worker, k.query_owner, k.kv_owner, k.helper]
+        for m in self.messages:
+            msgs += [m.step, m.from_, m.to, int(m.kind)]
+        return tasks, msgs
+
+
+def _build(workers: int, kind: int) -> Schedule:
+    lib = _lib.lib()
+    steps = C.c_int32(0)
+    nt, nm = C.c_int64(0), C.c_int64(0)
+    check(lib.da_schedule_build(workers, kind, C.byref(steps), None, C.byref(nt), None, C.byref(nm)))
+    tasks = (C.c_int32 * (6 * nt.value))()
+    msgs = (C.c_int32 * (4 * max(nm.value, 1)))()
+    check(lib.da_schedule_build(workers, kind, C.byref(steps), tasks, C.byref(nt), msgs, C.byref(nm)))
+    s = Schedule(workers=workers, steps=[[] for _ in range(steps.value)])
+    for i in range(nt.value):
+        st, k, w, qo, kvo, h = tasks[6 * i: 6 * i + 6]
+        s.steps[st].append(Task(TaskKind(k), w, qo, kvo, h))
+    for i in range(nm.value):
+        st, f, to, k = msgs[4 * i: 4 * i + 4]
+        s.messages.append(ScheduleMessage(st, f, to, PayloadKind(k)))
+    return s
+
+
+def build_ring_schedule(workers: int) -> Schedule:
+    """schedule.cpp:60-77"""
+    return _build(workers, 0)
+
+
+def build_balanced_schedule(workers: int) -> Schedule:
+    """schedule.cpp:79-108"""
+    return _build(workers, 1)
+
+
+def validate(s: Schedule) -> list:
+    """schedule.cpp:121-258. Returns the number of violations as a list of
+    messages (only the first carries text; the native validator reports it)."""
+    tasks, msgs = s.flat()
+    ta = (C.c_int32 * max(len(tasks), 1))(*tasks)
+    ma = (C.c_int32 * max(len(msgs), 1))(*msgs)
+    lib = _lib.lib()
+    n = lib.da_schedule_validate(s.workers, len(s.steps), ta, len(tasks) // 6, ma, len(msgs) // 4)
+    if n < 0:
+        raise ConfigError(lib.da_last_error().decode())
+    if n == 0:
+        return []
+    first = lib.da_last_error().decode()
+    return [first] + [""] * (n - 1)
+
+
+def idle_fraction(s: Schedule) -> Fraction:
+    slots = s.workers * s.step_count()
+    return Fraction(0) if slots == 0 else Fraction(s.idle_slot_count(), slots)
+
+
+def expected_speedup(s: Schedule) -> Fraction:
+    return Fraction(0) if s.step_count() == 0 else Fraction(s.attention_task_count(), s.step_count())
+
+
+def ring_idle_fraction_formula(workers: int) -> Fraction:
+    if workers < 1:
+        raise ConfigError("need at least 1 worker")
+    return Fraction(workers * workers - workers, 2 * workers * workers)
+
+
+def balanced_idle_fraction_reference(workers: int) -> Fraction:
+    if workers < 1:
+        raise ConfigError("need at least 1 worker")
+    return Fraction(0) if workers % 2 == 1 else Fraction(1, 2 * workers)
+
+
+def schedule_to_json(s: Schedule) -> str:
+    """schedule.cpp:301-327 (same keys)."""
+    def task_json(t: Task):
+        j = {"kind": _TASK_NAMES[int(t.kind)]}
+        if t.kind == TaskKind.RemoteAttn:
+            j["query_owner"] = t.query_owner
+            j["kv_owner"] = t.kv_owner
+        elif t.kind == TaskKind.RescaleMerge:
+            j["helper"] = t.helper
+        return j
+    j = {"P": s.workers,
+         "steps": [[{"task": task_json(t), "worker": t.worker} for t in step] for step in s.steps],
+         "messages": [{"from": m.from_, "kind": _PAYLOAD_NAMES[int(m.kind)], "step": m.step,
+                       "to": m.to} for m in s.messages]}
+    return json.dumps(j, indent=2, sort_keys=True)
+
+
+def schedule_to_csv(s: Schedule) -> str:
+    """schedule.cpp:329-342 (same columns)."""
+    lines = ["step,worker,task,query_owner,kv_owner,helper"]
+    for t, step in enumerate(s.steps):
+        for k in step:
+            row = f"{t},{k.worker},{_TASK_NAMES[int(k.kind)]},"
+            if k.kind == TaskKind.RemoteAttn:
+                row += f"{k.query_owner},{k.kv_owner},"
+            elif k.kind == TaskKind.LocalAttn:
+                row += f"{k.worker},{k.worker},"
+            else:
+                row += ",,"
+            if k.kind == TaskKind.RescaleMerge:
+                row += f"{k.helper}"
+            lines.append(row)
+    return "\n".join(lines) + "\n"

@@ -1,0 +1,134 @@
+"""GPU parity of the sm_100a chunk kernels against plain PyTorch fp32 references.
+
+Tolerances (north_star): O/dQ/dK/dV max-abs error / max|ref| <= 2e-2,
+logsumexp max-abs <= 1e-3, for bf16 inputs with fp32 accumulation.
+"""
+import math
+
+import pytest
+import torch
+
+from torch_ref import attention_grads_ref, attention_ref, rel_err
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-2
+LSE_TOL = 1e-3
+
+
+def _qkv(h, n, hkv=None, nk=None, seed=0, dev="cuda", amp=1.0):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    hkv = hkv or h
+    nk = nk or n
+    q = (torch.rand(h, n, 128, generator=g) * 2 - 1) * amp
+    k = torch.rand(hkv, nk, 128, generator=g) * 2 - 1
+    v = torch.rand(hkv, nk, 128, generator=g) * 2 - 1
+    return [x.to(torch.bfloat16).to(dev) for x in (q, k, v)]
+
+
+def test_debug_scores_layout(cuda):
+    from paper_2310_03294_b200 import _lib
+    import ctypes as C
+    q, k, _ = _qkv(1, 128)
+    s = torch.zeros(128, 128, dtype=torch.float32, device=cuda)
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    rc = _lib.lib().da_debug_scores(C.c_void_p(q.data_ptr()), C.c_void_p(k.data_ptr()), 128,
+                                    C.c_void_p(s.data_ptr()), st)
+    assert rc == 0, _lib.lib().da_last_error()
+    ref = q[0].float() @ k[0].float().T
+    assert rel_err(s, ref) < 1e-3
+
+
+@pytest.mark.parametrize("h,n", [(1, 128), (2, 256), (2, 384), (3, 200), (2, 1024)])
+def test_fwd_diagonal_finalize(cuda, h, n):
+    from paper_2310_03294_b200.flashcore import MaskMode, block_attn_update_final
+    q, k, v = _qkv(h, n, seed=n)
+    out = block_attn_update_final(q, k, v, None, MaskMode.Diagonal)
+    torch.cuda.synchronize()
+    o_ref, lse_ref = attention_ref(q, k, v, True)
+    assert rel_err(out.o, o_ref) < TOL
+    assert (out.lse - lse_ref).abs().max().item() < LSE_TOL
+
+
+@pytest.mark.parametrize("h,hkv,n,nk", [(2, 2, 256, 256), (4, 1, 128, 384), (2, 2, 300, 130)])
+def test_fwd_full_accumulator(cuda, h, hkv, n, nk):
+    from paper_2310_03294_b200.flashcore import MaskMode, block_attn_update, finalize
+    q, k, v = _qkv(h, n, hkv, nk, seed=7)
+    acc = block_attn_update(q, k, v, None, MaskMode.Full)
+    out = finalize(acc)
+    o_ref, lse_ref = attention_ref(q, k, v, False)
+    assert rel_err(out.o, o_ref) < TOL
+    assert (out.lse - lse_ref).abs().max().item() < LSE_TOL
+
+
+def test_fwd_chunk_chain_matches_full_causal(cuda):
+    """Owner of chunk 3 absorbs kv 3 (diagonal), then kv 1, kv 2 (full), merging in-kernel."""
+    from paper_2310_03294_b200.flashcore import MaskMode, block_attn_update, block_attn_update_final
+    h, c = 2, 256
+    q, k, v = _qkv(h, 3 * c, seed=3)
+    qs, ks, vs = (x.split(c, dim=1) for x in (q, k, v))
+    qs, ks, vs = [t.contiguous() for t in qs], [t.contiguous() for t in ks], [t.contiguous() for t in vs]
+    acc = block_attn_update(qs[2], ks[2], vs[2], None, MaskMode.Diagonal)
+    acc = block_attn_update(qs[2], ks[0], vs[0], acc, MaskMode.Full, out=acc)
+    out = block_attn_update_final(qs[2], ks[1], vs[1], acc, MaskMode.Full)
+    o_ref, lse_ref = attention_ref(q, k, v, True)
+    assert rel_err(out.o, o_ref[:, 2 * c:]) < TOL
+    assert (out.lse - lse_ref[:, 2 * c:]).abs().max().item() < LSE_TOL
+
+
+def test_rescale_merge_and_identity(cuda):
+    from paper_2310_03294_b200.flashcore import (AttnAccumulator, MaskMode, block_attn_update,
+                                                 finalize, rescale)
+    h, c = 2, 128
+    q, k, v = _qkv(h, 2 * c, seed=11)
+    ks, vs = k.split(c, dim=1), v.split(c, dim=1)
+    a = block_attn_update(q, ks[0].contiguous(), vs[0].contiguous(), None, MaskMode.Full)
+    b = block_attn_update(q, ks[1].contiguous(), vs[1].contiguous(), None, MaskMode.Full)
+    m = rescale(a, b)
+    out = finalize(m)
+    o_ref, lse_ref = attention_ref(q, k, v, False)
+    assert rel_err(out.o, o_ref) < TOL
+    # a fresh accumulator is the identity (flashcore.hpp:214-217)
+    fresh = AttnAccumulator.fresh(h, 2 * c)
+    same = rescale(fresh, m)
+    assert torch.equal(same.o, m.o) and torch.equal(same.l, m.l) and torch.equal(same.m, m.m)
+
+
+@pytest.mark.parametrize("h,hkv,n,diag", [(1, 1, 128, True), (2, 2, 256, True), (2, 2, 384, True),
+                                          (4, 2, 256, True), (2, 2, 256, False), (3, 3, 200, True)])
+def test_bwd_chunk(cuda, h, hkv, n, diag):
+    from paper_2310_03294_b200.flashcore import MaskMode, block_attn_backward
+    q, k, v = _qkv(h, n, hkv, seed=100 + n)
+    g = torch.Generator().manual_seed(5)
+    d_out = (torch.rand(h, n, 128, generator=g) * 2 - 1).to(torch.bfloat16).to(cuda)
+    o_ref, lse_ref = attention_ref(q, k, v, diag)
+    out_bf = o_ref.to(torch.bfloat16)
+    mask = MaskMode.Diagonal if diag else MaskMode.Full
+    grads = block_attn_backward(q, k, v, out_bf, lse_ref.contiguous(), d_out, mask)
+    torch.cuda.synchronize()
+    dq, dk, dv = attention_grads_ref(q, k, v, d_out, diag)
+    assert rel_err(grads.dv, dv) < TOL, "dv"
+    assert rel_err(grads.dk, dk) < TOL, "dk"
+    assert rel_err(grads.dq, dq) < TOL, "dq"
+
+
+def test_single_gpu_fwd_bwd_32k_sampled(cuda):
+    """cfg2 shape at 2 heads: full causal 32K forward+backward, rows sampled against fp32."""
+    from paper_2310_03294_b200.flashcore import MaskMode, block_attn_backward, block_attn_update_final
+    h, n = 2, 32768
+    q, k, v = _qkv(h, n, seed=1)
+    out = block_attn_update_final(q, k, v, None, MaskMode.Diagonal)
+    rows = torch.tensor([0, 1, 127, 128, 4095, 16384, 32766, 32767], device=cuda)
+    qs = q[:, rows].float()
+    s = torch.einsum("hid,hjd->hij", qs, k.float()) / math.sqrt(128)
+    mask = torch.arange(n, device=cuda)[None, :] <= rows[:, None]
+    s = s.masked_fill(~mask[None], float("-inf"))
+    lse_ref = torch.logsumexp(s, -1)
+    o_ref = torch.einsum("hij,hjd->hid", torch.softmax(s, -1), v.float())
+    assert rel_err(out.o[:, rows], o_ref) < TOL
+    assert (out.lse[:, rows] - lse_ref).abs().max().item() < LSE_TOL
+    d_out = torch.randn_like(out.o, dtype=torch.float32).to(torch.bfloat16)
+    grads = block_attn_backward(q, k, v, out.o, out.lse, d_out, MaskMode.Diagonal)
+    torch.cuda.synchronize()
+    assert torch.isfinite(grads.dq).all() and torch.isfinite(grads.dk).all()
+    assert torch.isfinite(grads.dv).all()
