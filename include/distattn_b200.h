@@ -159,8 +159,9 @@ typedef enum da_schedule_kind { DA_SCHEDULE_RING = 0, DA_SCHEDULE_BALANCED = 1 }
 da_status da_schedule_build(int workers, int kind, int32_t* steps_out, int32_t* tasks,
                             int64_t* n_tasks, int32_t* messages, int64_t* n_messages);
 
-/* validate (schedule.cpp:121-258): returns the violation count; writes the
- * first message into da_last_error() when nonzero. Negative on bad input. */
+/* validate (schedule.cpp:121-258): returns the violation count; when nonzero
+ * da_last_error() holds every violation message, newline-separated.
+ * Negative on bad input. */
 int64_t da_schedule_validate(int workers, int32_t steps, const int32_t* tasks, int64_t n_tasks,
                              const int32_t* messages, int64_t n_messages);
 

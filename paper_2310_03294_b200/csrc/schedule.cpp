@@ -237,7 +237,11 @@ int64_t da_schedule_validate(int workers, int32_t steps, const int32_t* tasks, i
     s.messages.push_back({o[0], o[1], o[2], o[3]});
   }
   const auto errs = da::validate_flat(s);
-  if (!errs.empty()) da::set_error(DA_ERR_SCHEDULE, errs.front());
+  if (!errs.empty()) {
+    std::string all;
+    for (const auto& e : errs) all += (all.empty() ? "" : "\n") + e;
+    da::set_error(DA_ERR_SCHEDULE, all);
+  }
   return static_cast<int64_t>(errs.size());
 }
 

@@ -118,8 +118,7 @@ def build_balanced_schedule(workers: int) -> Schedule:
 
 
 def validate(s: Schedule) -> list:
-    """schedule.cpp:121-258. Returns the number of violations as a list of
-    messages (only the first carries text; the native validator reports it)."""
+    """schedule.cpp:121-258: the list of violation messages (empty = valid)."""
     tasks, msgs = s.flat()
     ta = (C.c_int32 * max(len(tasks), 1))(*tasks)
     ma = (C.c_int32 * max(len(msgs), 1))(*msgs)
@@ -129,8 +128,9 @@ def validate(s: Schedule) -> list:
         raise ConfigError(lib.da_last_error().decode())
     if n == 0:
         return []
-    first = lib.da_last_error().decode()
-    return [first] + [""] * (n - 1)
+    msgs = lib.da_last_error().decode().split("\n")
+    assert len(msgs) == n, (n, msgs)
+    return msgs
 
 
 def idle_fraction(s: Schedule) -> Fraction:
