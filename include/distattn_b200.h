@@ -201,6 +201,14 @@ da_status da_run_backward(const da_shards* shards, da_counters* counters, void* 
 /* Frees the cached runtime workspace of the calling thread. */
 void da_runtime_release(void);
 
+/* Device fill with the reference's splitmix64 stream (numerics.hpp:140-174):
+ * out[i] = lo + (hi - lo) * unit(draw i of the stream whose CURRENT state is
+ * `state`), stored as dtype 0 = fp32, 1 = bf16 (via fp32, round-to-nearest-
+ * even), 2 = fp64. The caller advances its state by n * 0x9E3779B97F4A7C15.
+ * Used by make_shards (runtime.cpp:24-46) to build parity inputs on device. */
+da_status da_rng_uniform(uint64_t state, int64_t n, double lo, double hi, int dtype, void* out,
+                         void* stream);
+
 /* Debug: compute the raw score block S = q kᵀ (fp32, unscaled) of the first
  * 128x128 tile of head 0 through the forward kernel's MMA path. */
 da_status da_debug_scores(const void* q, const void* k, int64_t rows, float* s_out, void* stream);

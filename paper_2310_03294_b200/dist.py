@@ -1,0 +1,393 @@
+"""One process per GPU: sequence-parallel causal attention over NCCL.
+
+The per-rank plan comes from the native schedule (csrc/schedule.cpp, bit-exact
+with schedule.cpp:60-108); the operation order per worker is the reference's
+(runtime.cpp:266-330 forward, :605-651 backward):
+
+forward (ring or load-balanced), worker w at step t:
+    Local   — update(q_w, k_w, v_w, Diagonal)          (fresh accumulator)
+    Direct  — recv KV(r); update(q_w, k_r, v_r, Full)  (accumulator in place)
+    Help    — recv Q(o);  partial = update(q_o, k_w, v_w, Full, fresh); send Partial -> o
+    then merges at the owner: recv Partial(h); acc = rescale(acc, partial)
+    finally finalize -> out (bf16) and lse (fp32), the state the backward reuses
+    (rematerialization-aware checkpointing: the forward is never recomputed).
+backward (ring, BackwardMode::Vanilla), worker p at step t:
+    t = 0: grads(q_p, k_p, v_p, Diagonal)
+    t >= 1, p > t: recv KV(p - t); grads(q_p, k_r, v_r, Full); send GradKV -> r
+    worker r folds GradKV from r + t.
+
+Communication: every message is a point-to-point NCCL send/recv issued on a
+dedicated comm stream. Immutable operands (KV, Q) of step t+1 are posted while
+step t computes (prefetch depth 1, double-buffered receive slots — the
+reference's residency bound of 2, acceptance_main.cpp:414-444); the compute
+stream waits on the receive before the consuming kernel. Partials and GradKV
+leave right after the kernel that produced them.
+
+The compute backend is pluggable so the host logic runs on CPU under gloo in
+the test-suite; the production backend (CudaBackend) is the sm_100a library.
+"""
+from __future__ import annotations
+
+import math
+import os
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as tdist
+
+from .schedule import TaskKind, build_balanced_schedule, build_ring_schedule, validate
+from .errors import ConfigError, ScheduleError, StateError
+
+
+# ----------------------------------------------------------------------------- compute backend
+class CudaBackend:
+    """sm_100a kernels through the C ABI (flashcore)."""
+
+    acc_dtype = torch.float32
+    grad_dtype = torch.float32
+
+    def __init__(self, device):
+        from . import flashcore as F
+        self.F = F
+        self.device = device
+
+    def new_acc(self, h, rows, d, packed: torch.Tensor | None = None):
+        if packed is None:
+            packed = torch.empty(h * rows * (d + 2), dtype=self.acc_dtype, device=self.device)
+        o = packed[: h * rows * d].view(h, rows, d)
+        m = packed[h * rows * d: h * rows * (d + 1)].view(h, rows)
+        l = packed[h * rows * (d + 1):].view(h, rows)
+        return self.F.AttnAccumulator(o, m, l), packed
+
+    def update(self, q, k, v, acc_in, mask: str, out_acc):
+        F = self.F
+        mm = F.MaskMode.Diagonal if mask == "diagonal" else F.MaskMode.Full
+        return F.block_attn_update(q, k, v, acc_in, mm, out=out_acc)
+
+    def merge(self, acc, part):
+        return self.F.rescale(acc, part, out=acc)
+
+    def finalize(self, acc):
+        o = self.F.finalize(acc)
+        return o.o, o.lse
+
+    def bwd_aux(self, d_out, out):
+        return self.F.backward_aux(d_out, out)
+
+    def grads(self, q, k, v, out, lse, d_out, d_vec, mask: str, dq, dk, dv, accumulate_kv: bool):
+        F = self.F
+        mm = F.MaskMode.Diagonal if mask == "diagonal" else F.MaskMode.Full
+        F.block_attn_backward(q, k, v, out, lse, d_out, mm, d_vec=d_vec,
+                              grads=F.ChunkGrads(dq, dk, dv), accumulate_kv=accumulate_kv)
+
+    def add_(self, dst, src):
+        dst.add_(src)
+
+
+# ----------------------------------------------------------------------------- transport
+class Transport:
+    """Point-to-point messages over torch.distributed (NCCL on GPU, gloo on CPU).
+
+    Ranks are 0-based; schedule workers are rank + 1."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.nccl = tdist.get_backend(group) == "nccl"
+        self.stream = torch.cuda.Stream() if self.nccl else None
+
+    def exchange(self, sends, recvs):
+        """Posts sends [(tensor, dst_rank)] and recvs [(tensor, src_rank)] as one
+        group. On NCCL the group starts only after everything already enqueued
+        on the current (compute) stream — so send data is produced and receive
+        slots are no longer read — and the returned handle's wait() orders the
+        current stream after the whole group. On gloo wait() blocks."""
+        if not sends and not recvs:
+            return _Done()
+        if self.nccl:
+            ready = torch.cuda.Event()
+            ready.record()
+            with torch.cuda.stream(self.stream):
+                self.stream.wait_event(ready)
+                ops = [tdist.P2POp(tdist.isend, t, r, self.group) for t, r in sends] + \
+                      [tdist.P2POp(tdist.irecv, t, r, self.group) for t, r in recvs]
+                works = tdist.batch_isend_irecv(ops)
+            return _Works(works)
+        works = [tdist.isend(t, r, self.group) for t, r in sends] + \
+                [tdist.irecv(t, r, self.group) for t, r in recvs]
+        return _Works(works)
+
+
+class _Done:
+    def wait(self):
+        pass
+
+
+class _Works:
+    def __init__(self, works):
+        self.works = works
+
+    def wait(self):
+        for w in self.works:
+            w.wait()
+
+
+# ----------------------------------------------------------------------------- plans
+@dataclass
+class StepPlan:
+    action: str = "idle"     # idle | local | direct | help
+    peer: int = 0            # 1-based: kv owner (direct) or query owner (help)
+    kv_sends: tuple = ()     # destinations (1-based) of my KV this step
+    q_sends: tuple = ()      # destinations of my Q this step
+    merges: tuple = ()       # helpers (1-based) whose partial I merge this step, in order
+
+
+def forward_plan(schedule, worker: int) -> list[StepPlan]:
+    """Per-worker view of a validated schedule (runtime.cpp:138-177)."""
+    plans = []
+    for t, step in enumerate(schedule.steps):
+        p = StepPlan()
+        for task in step:
+            if task.worker != worker:
+                continue
+            if task.kind == TaskKind.LocalAttn:
+                p.action = "local"
+            elif task.kind == TaskKind.RemoteAttn:
+                if task.query_owner == worker:
+                    p.action, p.peer = "direct", task.kv_owner
+                else:
+                    p.action, p.peer = "help", task.query_owner
+            elif task.kind == TaskKind.RescaleMerge:
+                p.merges += (task.helper,)
+        p.kv_sends = tuple(m.to for m in schedule.messages
+                           if m.step == t and m.from_ == worker and int(m.kind) == 0)
+        p.q_sends = tuple(m.to for m in schedule.messages
+                          if m.step == t and m.from_ == worker and int(m.kind) == 1)
+        plans.append(p)
+    return plans
+
+
+# ----------------------------------------------------------------------------- runtime
+class DistRuntime:
+    """Sequence-parallel attention for ONE rank holding chunk `rank` of the sequence.
+
+    q/k/v: [heads, rows, d] (bf16 on GPU). Call forward() then backward(d_out).
+    """
+
+    def __init__(self, rank: int, world: int, backend=None, transport=None, device=None):
+        self.rank, self.world = rank, world
+        self.worker = rank + 1
+        self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.backend = backend if backend is not None else CudaBackend(self.device)
+        self.transport = transport if transport is not None else Transport()
+        if self.transport.nccl and world > 1:
+            # the first P2P batch must not be the group's first collective
+            warm = torch.zeros(1, device=self.device)
+            tdist.all_reduce(warm, group=self.transport.group)
+        self.saved = None
+        self.trace = {"messages_sent": 0, "bytes_sent": 0, "max_remote_chunks_held": 0}
+        self._bufs = {}
+
+    # -- buffers (allocated once per shape; not on the steady-state hot path)
+    def _buf(self, key, shape, dtype):
+        t = self._bufs.get(key)
+        if t is None or t.shape != torch.Size(shape) or t.dtype != dtype:
+            t = torch.empty(shape, dtype=dtype, device=self.device)
+            self._bufs[key] = t
+        return t
+
+    def _sent(self, *tensors):
+        self.trace["messages_sent"] += 1
+        self.trace["bytes_sent"] += sum(t.numel() * t.element_size() for t in tensors)
+
+    def forward(self, q, k, v, schedule: str = "balanced", overlap: bool = True):
+        P, w = self.world, self.worker
+        sched = build_balanced_schedule(P) if schedule == "balanced" else build_ring_schedule(P)
+        viol = validate(sched)
+        if viol:
+            raise ScheduleError(f"invalid schedule: {viol[0]} ({len(viol)} violations)")
+        plans = forward_plan(sched, w)
+        h, rows, d = q.shape
+        hk = k.shape[0]
+        be, tr = self.backend, self.transport
+        acc, _ = be.new_acc(h, rows, d, self._buf("acc", (h * rows * (d + 2),), be.acc_dtype))
+        have_acc = False
+        # receive slots: double-buffered (prefetch depth 1)
+        kv_slot = [(self._buf(f"k{i}", (hk, rows, d), k.dtype), self._buf(f"v{i}", (hk, rows, d), v.dtype))
+                   for i in range(2)]
+        q_slot = [self._buf(f"q{i}", (h, rows, d), q.dtype) for i in range(2)]
+        part_pk = self._buf("part_send", (h * rows * (d + 2),), be.acc_dtype)
+        part, _ = be.new_acc(h, rows, d, part_pk)
+        recv_part = {}
+
+        def post_operands(t):
+            """sends of my immutable KV/Q for step t + the receive my step-t action needs."""
+            p = plans[t]
+            sends, recvs = [], []
+            for dst in p.kv_sends:
+                sends += [(k, dst - 1), (v, dst - 1)]
+                self._sent(k, v)
+            for dst in p.q_sends:
+                sends.append((q, dst - 1))
+                self._sent(q)
+            if p.action == "direct":
+                ks, vs = kv_slot[t % 2]
+                recvs += [(ks, p.peer - 1), (vs, p.peer - 1)]
+            elif p.action == "help":
+                recvs.append((q_slot[t % 2], p.peer - 1))
+            return tr.exchange(sends, recvs)
+
+        held = 0
+        part_handle = None
+        pending = post_operands(0) if P > 1 else _Done()
+        for t, p in enumerate(plans):
+            handle = pending
+            nxt = None
+            if overlap and t + 1 < len(plans):
+                nxt = post_operands(t + 1)  # prefetch: overlaps this step's compute
+            handle.wait()
+            cur_held = (1 if p.action in ("direct", "help") else 0) + (1 if nxt is not None and plans[t + 1].action in ("direct", "help") else 0)
+            held = max(held, cur_held)
+            if p.action == "local":
+                be.update(q, k, v, acc if have_acc else None, "diagonal", acc)
+                have_acc = True
+            elif p.action == "direct":
+                ks, vs = kv_slot[t % 2]
+                be.update(q, ks, vs, acc if have_acc else None, "full", acc)
+                have_acc = True
+            elif p.action == "help":
+                if part_handle is not None:
+                    part_handle.wait()  # the previous partial has left this buffer
+                be.update(q_slot[t % 2], k, v, None, "full", part)
+                part_handle = tr.exchange([(part_pk, p.peer - 1)], [])
+                self._sent(part_pk)
+            # merges of partials computed by helpers this step
+            for hw in p.merges:
+                buf = recv_part.get(hw)
+                if buf is None:
+                    buf = self._buf(f"part_recv{hw}", (h * rows * (d + 2),), be.acc_dtype)
+                    recv_part[hw] = buf
+                tr.exchange([], [(buf, hw - 1)]).wait()
+                pa, _ = be.new_acc(h, rows, d, buf)
+                be.merge(acc, pa)
+            if not overlap and t + 1 < len(plans):
+                nxt = post_operands(t + 1)
+            pending = nxt if nxt is not None else _Done()
+        if part_handle is not None:
+            part_handle.wait()
+        self.trace["max_remote_chunks_held"] = held
+        out, lse = be.finalize(acc)
+        self.saved = (q, k, v, out, lse)
+        return out, lse
+
+    def backward(self, d_out, overlap: bool = True):
+        """Ring backward reusing the saved O and LSE (no forward recompute)."""
+        if self.saved is None:
+            raise StateError("run_backward requires forward output and logsumexp")
+        q, k, v, out, lse = self.saved
+        P, w = self.world, self.worker
+        h, rows, d = q.shape
+        hk = k.shape[0]
+        be, tr = self.backend, self.transport
+        dq = self._buf("dq", (h, rows, d), be.grad_dtype)
+        dk = self._buf("dk", (hk, rows, d), be.grad_dtype)
+        dv = self._buf("dv", (hk, rows, d), be.grad_dtype)
+        dq.zero_()
+        d_vec = be.bwd_aux(d_out, out)
+        kv_slot = [(self._buf(f"bk{i}", (hk, rows, d), k.dtype), self._buf(f"bv{i}", (hk, rows, d), v.dtype))
+                   for i in range(2)]
+        g_send = [(self._buf(f"gk{i}", (hk, rows, d), be.grad_dtype),
+                   self._buf(f"gv{i}", (hk, rows, d), be.grad_dtype)) for i in range(2)]
+        g_recv = (self._buf("grk", (hk, rows, d), be.grad_dtype),
+                  self._buf("grv", (hk, rows, d), be.grad_dtype))
+
+        def post_kv(t):
+            """step t >= 1: I send my KV to w + t; I receive KV of w - t."""
+            sends, recvs = [], []
+            if w + t <= P:
+                sends += [(k, w + t - 1), (v, w + t - 1)]
+                self._sent(k, v)
+            if w - t >= 1:
+                ks, vs = kv_slot[t % 2]
+                recvs += [(ks, w - t - 1), (vs, w - t - 1)]
+            return tr.exchange(sends, recvs)
+
+        be.grads(q, k, v, out, lse, d_out, d_vec, "diagonal", dq, dk, dv, accumulate_kv=False)
+        pending = post_kv(1) if P > 1 else _Done()
+        for t in range(1, P):
+            handle = pending
+            nxt = post_kv(t + 1) if (overlap and t + 1 < P) else None
+            handle.wait()
+            gsend = None
+            if w - t >= 1:
+                ks, vs = kv_slot[t % 2]
+                gk, gv = g_send[t % 2]
+                be.grads(q, ks, vs, out, lse, d_out, d_vec, "full", dq, gk, gv, accumulate_kv=False)
+                gsend = [(gk, w - t - 1), (gv, w - t - 1)]
+                self._sent(gk, gv)
+            grecv = [(g_recv[0], w + t - 1), (g_recv[1], w + t - 1)] if w + t <= P else []
+            # GradKV leaves right after its kernel; waiting also retires the send
+            # buffer before it is rewritten two steps later
+            tr.exchange(gsend or [], grecv).wait()
+            if grecv:
+                be.add_(dk, g_recv[0])
+                be.add_(dv, g_recv[1])
+            if not overlap and t + 1 < P:
+                nxt = post_kv(t + 1)
+            pending = nxt if nxt is not None else _Done()
+        return dq, dk, dv
+
+
+# ----------------------------------------------------------------------------- bench (N > 1)
+def bench_main(args) -> int:
+    """torchrun entry for bench.py --gpus N: sequence-parallel fwd+bwd of the
+    Llama-7B attention layer at seq 32K x N (32K tokens per GPU, weak scaling),
+    balanced forward + ring backward over NCCL."""
+    import json
+    import statistics
+    import time
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    tdist.init_process_group("nccl", device_id=dev)
+    heads, d = args.heads, 128
+    rows = args.seq
+    n_total = rows * world
+    torch.manual_seed(1234 + rank)
+    q, k, v, do = [(torch.rand(heads, rows, d, device=dev) * 2 - 1).to(torch.bfloat16) for _ in range(4)]
+    rt = DistRuntime(rank, world, device=dev)
+
+    def step():
+        rt.forward(q, k, v, "balanced")
+        rt.backward(do)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    tdist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(args.steps):
+        step()
+    e.record()
+    torch.cuda.synchronize()
+    tdist.barrier()
+    ms = torch.tensor([s.elapsed_time(e) / args.steps], device=dev)
+    tdist.all_reduce(ms, op=tdist.ReduceOp.MAX)
+    ms = ms.item()
+    fl = 7.0 * n_total * n_total * d * heads
+    if rank == 0:
+        line = {"metric": "attn fwd+bwd TFLOP/s", "value": fl / (ms * 1e-3) / 1e12,
+                "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": {"workload": f"llama7b-attn causal fwd+bwd, 32 heads, d=128, seq "
+                                       f"{n_total} over {world} B200 (balanced fwd, ring bwd, NCCL)",
+                           "heads": heads, "d": d, "seq_len": n_total, "tokens_per_gpu": rows},
+                "tokens_per_s": n_total / (ms * 1e-3),
+                "tflops_per_gpu": fl / (ms * 1e-3) / 1e12 / world}
+        print(json.dumps(line), flush=True)
+    tdist.destroy_process_group()
+    return 0

@@ -1,0 +1,134 @@
+"""Multi-process host logic of the distributed runtime (dist.py) on CPU.
+
+world_size 2/3/4 over gloo with a TEST-ONLY compute backend built on the C
+oracle: the per-worker op order of DistRuntime is the reference's, so the
+results must be bit-identical to the oracle's single-process stepper (itself
+bit-exact with the reference build). The production path swaps in the sm_100a
+backend and NCCL; this test pins plan decoding, message routing, prefetch,
+partial merges and GradKV folding.
+"""
+import math
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as tdist
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+
+
+class OracleBackend:
+    acc_dtype = torch.float64
+    grad_dtype = torch.float64
+
+    def __init__(self, d):
+        self.scale = 1.0 / math.sqrt(d)
+
+    def new_acc(self, h, rows, d, packed=None):
+        if packed is None:
+            packed = torch.empty(h * rows * (d + 2), dtype=torch.float64)
+        o = packed[: h * rows * d].view(h, rows, d)
+        m = packed[h * rows * d: h * rows * (d + 1)].view(h, rows)
+        l = packed[h * rows * (d + 1):].view(h, rows)
+        return (o, m, l), packed
+
+    def update(self, q, k, v, acc_in, mask, out_acc):
+        h, hk = q.shape[0], k.shape[0]
+        for i in range(h):
+            prev = None if acc_in is None else tuple(x[i].numpy() for x in acc_in)
+            o, m, l = O.block_attn_update(q[i].numpy(), k[i * hk // h].numpy(),
+                                          v[i * hk // h].numpy(), prev, mask, self.scale)
+            out_acc[0][i].copy_(torch.from_numpy(o))
+            out_acc[1][i].copy_(torch.from_numpy(m))
+            out_acc[2][i].copy_(torch.from_numpy(l))
+        return out_acc
+
+    def merge(self, acc, part):
+        for i in range(acc[0].shape[0]):
+            o, m, l = O.rescale(tuple(x[i].numpy() for x in acc), tuple(x[i].numpy() for x in part))
+            acc[0][i].copy_(torch.from_numpy(o))
+            acc[1][i].copy_(torch.from_numpy(m))
+            acc[2][i].copy_(torch.from_numpy(l))
+        return acc
+
+    def finalize(self, acc):
+        outs, lses = [], []
+        for i in range(acc[0].shape[0]):
+            o, lse = O.finalize(tuple(x[i].numpy() for x in acc))
+            outs.append(torch.from_numpy(o))
+            lses.append(torch.from_numpy(lse))
+        return torch.stack(outs), torch.stack(lses)
+
+    def bwd_aux(self, d_out, out):
+        return None  # the oracle's block_attn_backward recomputes D (flashcore.hpp:294)
+
+    def grads(self, q, k, v, out, lse, d_out, d_vec, mask, dq, dk, dv, accumulate_kv):
+        h, hk = q.shape[0], k.shape[0]
+        if not accumulate_kv:
+            dk.zero_()
+            dv.zero_()
+        for i in range(h):
+            j = i * hk // h
+            gq, gk, gv = O.block_attn_backward(q[i].numpy(), k[j].numpy(), v[j].numpy(),
+                                               out[i].numpy(), lse[i].numpy(), d_out[i].numpy(),
+                                               mask, self.scale)
+            dq[i] += torch.from_numpy(gq)
+            dk[j] += torch.from_numpy(gk)
+            dv[j] += torch.from_numpy(gv)
+
+    def add_(self, dst, src):
+        dst.add_(src)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, n, d, heads, schedule, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2310_03294_b200.dist import DistRuntime, Transport
+        q, k, v, do = O.make_inputs(0, world, n, d, heads, bf16=True)
+        rows = n // world
+        sl = slice(rank * rows, (rank + 1) * rows)
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a[:, sl]))  # noqa: E731
+        rt = DistRuntime(rank, world, backend=OracleBackend(d), transport=Transport(),
+                         device=torch.device("cpu"))
+        out, lse = rt.forward(t(q), t(k), t(v), schedule)
+        dq, dk, dv = rt.backward(t(do))
+        np.savez(os.path.join(outdir, f"r{rank}.npz"), out=out.numpy(), lse=lse.numpy(),
+                 dq=dq.numpy(), dk=dk.numpy(), dv=dv.numpy(),
+                 held=rt.trace["max_remote_chunks_held"])
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,schedule", [(2, "balanced"), (3, "balanced"), (4, "balanced"),
+                                            (4, "ring")])
+def test_dist_runtime_gloo_bit_exact(world, schedule):
+    n, d, heads = 16 * world, 8, 2
+    with tempfile.TemporaryDirectory() as td:
+        mp.spawn(_worker, args=(world, _free_port(), n, d, heads, schedule, td), nprocs=world,
+                 join=True)
+        res = [np.load(os.path.join(td, f"r{r}.npz")) for r in range(world)]
+    q, k, v, do = O.make_inputs(0, world, n, d, heads, bf16=True)
+    for h in range(heads):
+        out, lse, _ = O.run_forward(q[h], k[h], v[h], world, schedule)
+        dq, dk, dv, _ = O.run_backward(q[h], k[h], v[h], out, lse, do[h], world)
+        got = {f: np.concatenate([r[f][h] for r in res], 0) for f in ("out", "lse", "dq", "dk", "dv")}
+        assert np.array_equal(got["out"], out)
+        assert np.array_equal(got["lse"], lse)
+        assert np.array_equal(got["dq"], dq)
+        assert np.array_equal(got["dk"], dk)
+        assert np.array_equal(got["dv"], dv)
+    assert max(int(r["held"]) for r in res) <= 2  # residency bound with prefetch
