@@ -209,6 +209,10 @@ void da_runtime_release(void);
 da_status da_rng_uniform(uint64_t state, int64_t n, double lo, double hi, int dtype, void* out,
                          void* stream);
 
+/* Debug: device buffer (64 x 16 uint64) receiving the backward kernel's
+ * per-iteration clock64 timeline of CTA 0 in DA_TRACE builds; NULL disables. */
+void da_debug_set_bwd_trace(void* buf);
+
 /* Debug: compute the raw score block S = q kᵀ (fp32, unscaled) of the first
  * 128x128 tile of head 0 through the forward kernel's MMA path. */
 da_status da_debug_scores(const void* q, const void* k, int64_t rows, float* s_out, void* stream);

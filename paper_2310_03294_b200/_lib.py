@@ -67,6 +67,7 @@ SIGNATURES = {
     "da_run_backward": (C.c_int, [C.POINTER(Shards), C.POINTER(Counters), vp]),
     "da_runtime_release": (None, []),
     "da_rng_uniform": (C.c_int, [C.c_uint64, i64, C.c_double, C.c_double, C.c_int, vp, vp]),
+    "da_debug_set_bwd_trace": (None, [vp]),
     "da_debug_scores": (C.c_int, [vp, vp, i64, vp, vp]),
 }
 

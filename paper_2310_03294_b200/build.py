@@ -16,13 +16,18 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-BUILD = PKG / "_build"
-LIB = PKG / "libdistattn_b200.so"
+BUILD = Path(os.environ.get("DA_BUILD_DIR", PKG / "_build"))
+LIB = Path(os.environ.get("DA_LIB_OUT", PKG / "libdistattn_b200.so"))
+EXTRA = os.environ.get("DA_BUILD_DEFINES", "").split()
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
               "-Xcompiler", "-fvisibility=hidden", "-DNDEBUG", "-I", str(ROOT / "include"),
               "-I", str(CSRC)]
+
+
+# kernels that redistribute registers with setmaxnreg need a known launch budget
+PER_FILE = {"attn_bwd_sm100.cu": ["-maxrregcount=128"]}
 
 
 def nvcc() -> str:
@@ -47,7 +52,8 @@ def _newest(paths) -> float:
 
 def _compile(src: Path, verbose: bool, ptxas_v: bool) -> Path:
     obj = BUILD / (src.name + ".o")
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *PER_FILE.get(src.name, []), *EXTRA, "-c", str(src), "-o",
+           str(obj)]
     if ptxas_v and src.suffix == ".cu":
         cmd += ["-Xptxas", "-v"]
     if verbose:

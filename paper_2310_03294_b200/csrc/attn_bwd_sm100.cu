@@ -11,14 +11,16 @@
 //   warp 4-11  compute: P, dS for (kv row = TMEM lane, 64 query columns each)
 //   warp 12    MMA issuer (one thread)
 //   warp 13    loader: TMA for K/V (once), Q (2 stages), dO (1 stage); lse/D rows
+//   warp 14-15 idle (complete the warpgroup for setmaxnreg)
 // TMEM (512 cols): dV [0,128) dK [128,256) S|P [256,384) dP|dS|dQ^T [384,512)
 //   S^T  = K Q^T          (SS, M=kv,  N=q)  -> S region
 //   dP^T = V dO^T         (SS, M=kv,  N=q)  -> dP region
 //   dV  += P^T dO         (TS, A = P^T in TMEM, B = dO MN-major)
 //   dK  += dS^T Q         (TS, A = dS^T in TMEM, B = Q MN-major)
 //   dQ^T = K^T dS^T       (SS, A = K MN-major, B = dS^T smem MN-major) -> dP region
-// Computing dQ transposed puts the head dim on TMEM lanes, so the drain warp
-// writes 32 consecutive floats of one dQ row per instruction (128 B).
+// Computing dQ transposed puts the head dim on TMEM lanes, so a drain warp
+// reduces 32 consecutive floats of one dQ row per instruction (128 B): per-row
+// 16-byte vector atomics were measured 25% slower (uncoalesced transactions).
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -28,12 +30,26 @@
 namespace da {
 namespace bwd {
 
+#ifdef DA_TRACE
+// slot layout per iteration (16 stamps): MMA 0-4, compute 5-8, drain 9-11
+#define BWD_TRACE(cond, it, slot)                                                       \
+  do {                                                                                  \
+    if ((cond) && p.trace != nullptr && blockIdx.x == 0 && (it) < 64)                   \
+      p.trace[(it) * 16 + (slot)] = clock64();                                          \
+  } while (0)
+#else
+#define BWD_TRACE(cond, it, slot) \
+  do {                            \
+  } while (0)
+#endif
+
 constexpr int kBM = 128;  // query rows per iteration
 constexpr int kBN = 128;  // kv rows per CTA
 constexpr int kHD = 128;
 constexpr uint32_t kTileBytes = 128 * 128 * 2;
 constexpr uint32_t kHalfTile = kTileBytes / 2;
-constexpr int kThreads = 448;
+constexpr int kThreads = 512;     // 4 warpgroups: drain | compute | compute | MMA+loader
+constexpr int kLaunchRegs = 128;  // the setmaxnreg budget below assumes exactly this
 constexpr uint32_t kColS = 256;
 constexpr uint32_t kColDP = 384;
 
@@ -123,6 +139,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
+
+  // Register redistribution (setmaxnreg is warpgroup-granular; every warp
+  // launches with kLaunchRegs = 128, 512 x 128 = 65536): WG3 (MMA, loader,
+  // two idle warps) 128 -> 96 releases 4 x 32 x 32 = 4096; the drain WG takes
+  // 4 x 32 x 16 = 2048 (-> 144) and the two compute WGs 8 x 32 x 8 = 2048 (-> 136).
+  if (warp >= 12) setmaxnreg_dec<96>();
 
   auto it_head = [&](int it) { return kv_head * group + it / n_i; };
   auto it_qtile = [&](int it) { return i0 + it % n_i; };
@@ -218,7 +240,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int st = it & 1;
         const bool has_next = it + 1 < n_it;
         // dV += P^T dO
+        BWD_TRACE(true, it, 0);
         mbar_wait(&bars->p_full, it & 1);
+        BWD_TRACE(true, it, 1);
         tc_fence_after();
         gemm_ts(tmem + 0, tmem + kColS, do_addr, it > 0);
         mma_commit(&bars->do_empty);
@@ -232,10 +256,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // dK += dS^T Q
         mbar_wait(&bars->ds_full, it & 1);
+        BWD_TRACE(true, it, 2);
         tc_fence_after();
         gemm_ts(tmem + 128, tmem + kColDP, q_addr + st * kTileBytes, it > 0);
         mma_commit(&bars->q_empty[st]);
-        // dQ^T = K^T dS^T  (A = K MN-major, B = dS^T MN-major)
+        // dQ^T = K^T dS^T  (A = K MN-major, B = dS^T MN-major): head dim on lanes
 #pragma unroll
         for (int kk = 0; kk < kBN / 16; ++kk) {
           mma_ss(tmem + kColDP, make_sdesc_sw128(k_addr + kk * 2048, kHalfTile, 1024),
@@ -246,7 +271,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // next dP^T once dQ^T has left TMEM
         if (has_next) {
           mbar_wait(&bars->dq_drained, it & 1);
+          BWD_TRACE(true, it, 3);
           mbar_wait(&bars->do_full, (it + 1) & 1);
+          BWD_TRACE(true, it, 4);
           tc_fence_after();
           gemm_kk(tmem + kColDP, v_addr, do_addr);
           mma_commit(&bars->dp_full);
@@ -254,35 +281,50 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mma_commit(&bars->acc_full);
     }
+  } else if (warp >= 14) {
+    // idle warps of the MMA/loader warpgroup
   } else if (warp < 4) {
     // ===================== dQ drain =====================
+    // all 128 columns are pulled out of TMEM before the region is released,
+    // so the next dP^T MMA waits only for the loads, not for the reductions
+    setmaxnreg_inc<144>();
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
     const int dcol = warp * 32 + lane;  // head-dim index = TMEM lane of dQ^T
     for (int it = 0; it < n_it; ++it) {
       const int hq = it_head(it);
       const int row0 = it_qtile(it) * kBM;
       mbar_wait(&bars->dq_full, it & 1);
+      BWD_TRACE(warp == 0 && lane == 0, it, 9);
       tc_fence_after();
+      uint32_t r[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(lane_base + kColDP + c * 32, r[c]);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&bars->dq_drained);
+      BWD_TRACE(warp == 0 && lane == 0, it, 10);
+      // a warp reduces 32 consecutive floats of one dQ row per instruction (128 B)
       float* base = p.dq_acc + (static_cast<size_t>(hq) * p.rows_q + row0) * kHD + dcol;
       const int q_valid = min(kBM, p.rows_q - row0);
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(lane_base + kColDP + c * 32, r);
-        tmem_ld_wait();
-        if (c == 3) {
-          tc_fence_before();
-          mbar_arrive(&bars->dq_drained);
-        }
+      if (q_valid == kBM) {
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const int q = c * 32 + k;
-          if (q < q_valid) red_add_f32(base + static_cast<size_t>(q) * kHD, p.scale * __uint_as_float(r[k]));
-        }
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int k = 0; k < 32; ++k)
+            red_add_f32(base + static_cast<size_t>(c * 32 + k) * kHD, p.scale * __uint_as_float(r[c][k]));
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int k = 0; k < 32; ++k)
+            if (c * 32 + k < q_valid)
+              red_add_f32(base + static_cast<size_t>(c * 32 + k) * kHD, p.scale * __uint_as_float(r[c][k]));
       }
+      BWD_TRACE(warp == 0 && lane == 0, it, 11);
     }
   } else {
     // ===================== compute (warps 4-11) =====================
+    setmaxnreg_inc<136>();
     const int cw = warp - 4;
     const int quarter = cw & 3;
     const int half = cw >> 2;
@@ -302,56 +344,57 @@ __global__ void __launch_bounds__(kThreads, 1)
 
       // ---- phase A: P = exp2(S * scale*log2e - lse2)
       mbar_wait(&bars->s_full, it & 1);
+      BWD_TRACE(cw == 0 && lane == 0, it, 5);
       tc_fence_after();
       uint32_t sr[2][32];
       tmem_ld_32x32b_x32(s_tmem, sr[0]);
       tmem_ld_32x32b_x32(s_tmem + 32, sr[1]);
       tmem_ld_wait();
-      float pr[64];
+      // P is carried to phase B as the same bf16 values the dV MMA consumes
+      uint32_t pk[32];
 #pragma unroll
       for (int c = 0; c < 64; c += 4) {
         const float4 l4 = *reinterpret_cast<const float4*>(lse2 + c);
-        pr[c + 0] = ex2_approx(fmaf(__uint_as_float(sr[c >> 5][(c + 0) & 31]), sl2, -l4.x));
-        pr[c + 1] = ex2_approx(fmaf(__uint_as_float(sr[c >> 5][(c + 1) & 31]), sl2, -l4.y));
-        pr[c + 2] = ex2_approx(fmaf(__uint_as_float(sr[c >> 5][(c + 2) & 31]), sl2, -l4.z));
-        pr[c + 3] = ex2_approx(fmaf(__uint_as_float(sr[c >> 5][(c + 3) & 31]), sl2, -l4.w));
+        float p0 = ex2_approx(fmaf(__uint_as_float(sr[c >> 5][(c + 0) & 31]), sl2, -l4.x));
+        float p1 = ex2_approx(fmaf(__uint_as_float(sr[c >> 5][(c + 1) & 31]), sl2, -l4.y));
+        float p2 = ex2_approx(fmaf(__uint_as_float(sr[c >> 5][(c + 2) & 31]), sl2, -l4.z));
+        float p3 = ex2_approx(fmaf(__uint_as_float(sr[c >> 5][(c + 3) & 31]), sl2, -l4.w));
+        if (diag) {
+          // query column (half*64 + c) is visible from kv row r iff q >= r
+          const int qc = half * 64 + c;
+          p0 = qc + 0 < r ? 0.f : p0;
+          p1 = qc + 1 < r ? 0.f : p1;
+          p2 = qc + 2 < r ? 0.f : p2;
+          p3 = qc + 3 < r ? 0.f : p3;
+        }
+        pk[c / 2] = pack_bf16x2(p0, p1);
+        pk[c / 2 + 1] = pack_bf16x2(p2, p3);
       }
-      if (diag) {
-        // query column (half*64 + c) is visible from kv row r iff q >= r
-#pragma unroll
-        for (int c = 0; c < 64; ++c)
-          if (half * 64 + c < r) pr[c] = 0.f;
-      }
-      {
-        uint32_t pk[32];
-#pragma unroll
-        for (int c = 0; c < 32; ++c) pk[c] = pack_bf16x2(pr[2 * c], pr[2 * c + 1]);
-        tmem_st_32x32b_x32(s_tmem, pk);
-      }
+      tmem_st_32x32b_x32(s_tmem, pk);
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&bars->p_full);
+      BWD_TRACE(cw == 0 && lane == 0, it, 6);
 
       // ---- phase B: dS = P o (dP - D)
       mbar_wait(&bars->dp_full, it & 1);
+      BWD_TRACE(cw == 0 && lane == 0, it, 7);
       tc_fence_after();
+      uint32_t dr[2][32];
+      tmem_ld_32x32b_x32(dp_tmem, dr[0]);
+      tmem_ld_32x32b_x32(dp_tmem + 32, dr[1]);
+      tmem_ld_wait();
       uint32_t dsk[32];
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        uint32_t dr[32];
-        tmem_ld_32x32b_x32(dp_tmem + hh * 32, dr);
-        tmem_ld_wait();
-#pragma unroll
-        for (int c = 0; c < 32; c += 4) {
-          const float4 d4 = *reinterpret_cast<const float4*>(dvec + hh * 32 + c);
-          const int b = hh * 32 + c;
-          const float s0 = pr[b + 0] * (__uint_as_float(dr[c + 0]) - d4.x);
-          const float s1 = pr[b + 1] * (__uint_as_float(dr[c + 1]) - d4.y);
-          const float s2 = pr[b + 2] * (__uint_as_float(dr[c + 2]) - d4.z);
-          const float s3 = pr[b + 3] * (__uint_as_float(dr[c + 3]) - d4.w);
-          dsk[(b >> 1) + 0] = pack_bf16x2(s0, s1);
-          dsk[(b >> 1) + 1] = pack_bf16x2(s2, s3);
-        }
+      for (int c = 0; c < 64; c += 4) {
+        const float4 d4 = *reinterpret_cast<const float4*>(dvec + c);
+        const uint32_t a = pk[c / 2], b = pk[c / 2 + 1];
+        const float s0 = __uint_as_float(a << 16) * (__uint_as_float(dr[c >> 5][(c + 0) & 31]) - d4.x);
+        const float s1 = __uint_as_float(a & 0xFFFF0000u) * (__uint_as_float(dr[c >> 5][(c + 1) & 31]) - d4.y);
+        const float s2 = __uint_as_float(b << 16) * (__uint_as_float(dr[c >> 5][(c + 2) & 31]) - d4.z);
+        const float s3 = __uint_as_float(b & 0xFFFF0000u) * (__uint_as_float(dr[c >> 5][(c + 3) & 31]) - d4.w);
+        dsk[c / 2] = pack_bf16x2(s0, s1);
+        dsk[c / 2 + 1] = pack_bf16x2(s2, s3);
       }
       // dS^T (bf16) -> TMEM (A operand of dK) and -> smem (B operand of dQ^T)
       tmem_st_32x32b_x32(dp_tmem, dsk);
@@ -365,6 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&bars->ds_full);
+      BWD_TRACE(cw == 0 && lane == 0, it, 8);
     }
 
     // ===================== epilogue: dV, dK rows =====================
@@ -429,6 +473,12 @@ cudaError_t launch_attn_bwd(const CUtensorMap& tq, const CUtensorMap& tk, const 
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(bwd::kSmemBytes));
     if (e != cudaSuccess) return e;
+    cudaFuncAttributes attr{};
+    e = cudaFuncGetAttributes(&attr, bwd::attn_bwd_kernel);
+    if (e != cudaSuccess) return e;
+    // setmaxnreg redistributes a fixed CTA budget; any other launch register
+    // count would make the drain warps' increase wait forever.
+    if (attr.numRegs != bwd::kLaunchRegs) return cudaErrorInvalidConfiguration;
     configured = true;
   }
   const int n_kv_tiles = (p.rows_kv + bwd::kBN - 1) / bwd::kBN;

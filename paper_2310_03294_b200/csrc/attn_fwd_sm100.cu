@@ -32,6 +32,11 @@ constexpr uint32_t kTileBytes = kBM * kHD * 2;  // 32 KB, one 128x128 bf16 tile
 constexpr uint32_t kHalfTile = kTileBytes / 2;  // one 64-column SW128 box
 constexpr int kThreads = 320;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+#ifndef DA_FWD_EX2_EMU_MOD
+#define DA_FWD_EX2_EMU_MOD 0
+#endif
+// every kEx2EmuMod-th pair of columns is exponentiated on the FMA pipe (0: none)
+constexpr int kEx2EmuMod = DA_FWD_EX2_EMU_MOD;
 
 struct SmemLayout {
   // all tiles 1024B aligned (SW128)
@@ -267,6 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(sr[c][i]));
       }
       mx *= sl2;
+      const bool masked_tile = diag || kv_valid < kBN;
 
       float alpha = 1.f;
       const float m_new = fmaxf(m_run, mx);
@@ -279,15 +285,32 @@ __global__ void __launch_bounds__(kThreads, 1)
 
       float rs = 0.f;
       uint32_t pk[2][32];
+      if (masked_tile || kEx2EmuMod == 0) {
+        // exact zeros for masked entries: MUFU only
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < 4; ++c)
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const float p0 = ex2_approx(fmaf(__uint_as_float(sr[c][i]), sl2, neg_m));
-          const float p1 = ex2_approx(fmaf(__uint_as_float(sr[c][i + 1]), sl2, neg_m));
-          rs += p0 + p1;
-          pk[c >> 1][(c & 1) * 16 + i / 2] = pack_bf16x2(p0, p1);
-        }
+          for (int i = 0; i < 32; i += 2) {
+            const float p0 = ex2_approx(fmaf(__uint_as_float(sr[c][i]), sl2, neg_m));
+            const float p1 = ex2_approx(fmaf(__uint_as_float(sr[c][i + 1]), sl2, neg_m));
+            rs += p0 + p1;
+            pk[c >> 1][(c & 1) * 16 + i / 2] = pack_bf16x2(p0, p1);
+          }
+      } else {
+        // steady state: every kEx2EmuMod-th column pair on the FMA pipe
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const float x0 = fmaf(__uint_as_float(sr[c][i]), sl2, neg_m);
+            const float x1 = fmaf(__uint_as_float(sr[c][i + 1]), sl2, neg_m);
+            const bool emu = kEx2EmuMod > 0 && ((c * 16 + i / 2) % kEx2EmuMod) == kEx2EmuMod - 1;
+            const float p0 = emu ? ex2_emu(x0) : ex2_approx(x0);
+            const float p1 = emu ? ex2_emu(x1) : ex2_approx(x1);
+            rs += p0 + p1;
+            pk[c >> 1][(c & 1) * 16 + i / 2] = pack_bf16x2(p0, p1);
+          }
+      }
       l_run = l_run * alpha + rs;
 
       // lazy O correction: only warps with a row whose max jumped

@@ -65,6 +65,8 @@ da_status make_tmap_3d(CUtensorMap* map, const void* base, int64_t heads, int64_
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+unsigned long long* g_bwd_trace = nullptr;
+
 }  // namespace da
 
 using da::set_error;
@@ -249,6 +251,7 @@ da_status da_attn_bwd_chunk(const da_bwd_args* a, void* stream) {
   p.dq_acc = a->dq_acc;
   p.dk_acc = a->dk_acc;
   p.dv_acc = a->dv_acc;
+  p.trace = da::g_bwd_trace;
   cudaError_t e = da::launch_attn_bwd(tq, tk, tv, tdo, p, st);
   return e == cudaSuccess ? DA_OK : da::cuda_error(e, "da_attn_bwd_chunk launch");
 }
@@ -258,6 +261,9 @@ da_status da_convert_f32_bf16(const float* src, void* dst, int64_t n, void* stre
   cudaError_t e = da::launch_convert(src, dst, n, reinterpret_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? DA_OK : da::cuda_error(e, "da_convert_f32_bf16");
 }
+
+// Debug (DA_TRACE builds only record): device buffer of 64*16 uint64 stamps.
+void da_debug_set_bwd_trace(void* buf) { da::g_bwd_trace = static_cast<unsigned long long*>(buf); }
 
 da_status da_debug_scores(const void* q, const void* k, int64_t rows, float* s_out, void* stream) {
   CUtensorMap tq, tk;

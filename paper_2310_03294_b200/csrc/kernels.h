@@ -37,6 +37,7 @@ struct BwdParams {
   float* dq_acc;
   float* dk_acc;
   float* dv_acc;
+  unsigned long long* trace;  // DA_TRACE builds: per-iteration clock64 stamps of CTA 0
 };
 
 cudaError_t launch_attn_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,

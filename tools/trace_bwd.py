@@ -1,0 +1,33 @@
+"""Prints the backward kernel's per-iteration clock64 timeline (CTA 0).
+Needs a DA_TRACE build: DISTATTN_B200_LIB=paper_2310_03294_b200/variants/lib_trace.so"""
+import ctypes as C
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2310_03294_b200 import _lib  # noqa: E402
+from paper_2310_03294_b200.flashcore import (ChunkGrads, MaskMode, backward_aux,  # noqa: E402
+                                             block_attn_backward, block_attn_update_final)
+
+h, n = 32, int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+q, k, v, do = [(torch.rand(h, n, 128, device="cuda") * 2 - 1).to(torch.bfloat16) for _ in range(4)]
+out = block_attn_update_final(q, k, v, None, MaskMode.Diagonal)
+dvec = backward_aux(do, out.o)
+g = ChunkGrads(torch.zeros(h, n, 128, device="cuda"), torch.empty(h, n, 128, device="cuda"),
+               torch.empty(h, n, 128, device="cuda"))
+tr = torch.zeros(64 * 16, dtype=torch.int64, device="cuda")
+_lib.lib().da_debug_set_bwd_trace(C.c_void_p(tr.data_ptr()))
+for _ in range(3):
+    block_attn_backward(q, k, v, out.o, out.lse, do, MaskMode.Diagonal, d_vec=dvec, grads=g)
+torch.cuda.synchronize()
+t = tr.view(64, 16).cpu().tolist()
+names = ["mma:wait_p", "mma:p_ok", "mma:ds_ok", "mma:drained", "mma:do_ok",
+         "cmp:A0", "cmp:A1", "cmp:B0", "cmp:B1", "drn:dq_ok", "drn:arrive", "drn:end"]
+base = t[0][0]
+for it in range(4, 16):
+    row = t[it]
+    t0 = row[1]
+    print(f"it {it:2d} period {t[it+1][1]-row[1]:6d}  " +
+          " ".join(f"{names[s]}={row[s]-t0:+6d}" for s in (2, 3, 4, 5, 6, 7, 8, 9, 10, 11)))
