@@ -27,6 +27,10 @@
 #include "kernels.h"
 #include "sm100_ptx.cuh"
 
+#ifndef DA_BWD_DQ_ATOMIC
+#define DA_BWD_DQ_TMA 1  // dQ reduced by TMA from smem (default); -DDA_BWD_DQ_ATOMIC: LSU red.add
+#endif
+
 namespace da {
 namespace bwd {
 
@@ -61,7 +65,12 @@ struct SmemLayout {
   static constexpr uint32_t ds = dout + kTileBytes;     // dS^T [kv][q] bf16, SW128 MN-major
   static constexpr uint32_t vecs = ds + kTileBytes;     // 2 stages x (lse2[128], D[128])
   static constexpr uint32_t bars = vecs + 2 * 2 * 128 * 4;
+#ifdef DA_BWD_DQ_TMA
+  static constexpr uint32_t dq_stage = bars + 1024;  // 4 warps x [32 q][32 d] fp32
+  static constexpr uint32_t total = dq_stage + 4 * 32 * 32 * 4;
+#else
   static constexpr uint32_t total = bars + 256;
+#endif
 };
 constexpr size_t kSmemBytes = SmemLayout::total + 1024;
 
@@ -69,6 +78,7 @@ struct Bars {
   uint64_t kv_full;
   uint64_t q_full[2];
   uint64_t q_empty[2];
+  uint64_t vec_full[2];
   uint64_t do_full;
   uint64_t do_empty;
   uint64_t s_full;
@@ -86,7 +96,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
                     const __grid_constant__ CUtensorMap tmap_k,
                     const __grid_constant__ CUtensorMap tmap_v,
-                    const __grid_constant__ CUtensorMap tmap_do, const BwdParams p) {
+                    const __grid_constant__ CUtensorMap tmap_do,
+                    const __grid_constant__ CUtensorMap tmap_dq, const BwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -113,6 +124,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int s = 0; s < 2; ++s) {
         mbar_init(&bars->q_full[s], 1);
         mbar_init(&bars->q_empty[s], 1);
+        mbar_init(&bars->vec_full[s], 1);
       }
       mbar_init(&bars->do_full, 1);
       mbar_init(&bars->do_empty, 1);
@@ -132,6 +144,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_prefetch_desc(&tmap_v);
       tma_prefetch_desc(&tmap_do);
     }
+  } else if (warp < 4) {
+    if (lane == 0) tma_prefetch_desc(&tmap_dq);
   } else if (warp == 12) {
     tmem_alloc<512>(&bars->tmem_base);
   }
@@ -165,35 +179,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int hq = it_head(it);
       const int row0 = it_qtile(it) * kBM;
       mbar_wait(&bars->q_empty[st], ph ^ 1);
-      // lse (log2 units) and D for the 128 query rows; padding rows get
-      // lse2 = +inf so their probabilities are exactly zero.
-      float* lse2 = vecs + st * 256;
-      float* dvec = lse2 + 128;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int r = lane * 4 + k;
-        const int row = row0 + r;
-        float l2 = INFINITY, dd = 0.f;
-        if (row < p.rows_q) {
-          const size_t idx = static_cast<size_t>(hq) * p.rows_q + row;
-          l2 = p.lse[idx] * kLog2e;
-          dd = p.d_vec[idx];
-        }
-        lse2[r] = l2;
-        dvec[r] = dd;
-      }
-      __syncwarp();
       if (lane == 0) {
         mbar_arrive_expect_tx(&bars->q_full[st], kTileBytes);
         uint8_t* qs = smem + SmemLayout::q + st * kTileBytes;
         tma_load_3d(qs, &tmap_q, &bars->q_full[st], 0, row0, hq);
         tma_load_3d(qs + kHalfTile, &tmap_q, &bars->q_full[st], 64, row0, hq);
+      }
+      // lse (log2 units) and D for the 128 query rows; padding rows get
+      // lse2 = +inf so their probabilities are exactly zero. The global loads
+      // stay in flight while the dO slot drains.
+      float l2[4], dd[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int row = row0 + lane * 4 + k;
+        l2[k] = INFINITY;
+        dd[k] = 0.f;
+        if (row < p.rows_q) {
+          const size_t idx = static_cast<size_t>(hq) * p.rows_q + row;
+          l2[k] = p.lse[idx] * kLog2e;
+          dd[k] = p.d_vec[idx];
+        }
+      }
+      if (lane == 0) {
         mbar_wait(&bars->do_empty, (it & 1) ^ 1);
         mbar_arrive_expect_tx(&bars->do_full, kTileBytes);
         tma_load_3d(smem + SmemLayout::dout, &tmap_do, &bars->do_full, 0, row0, hq);
         tma_load_3d(smem + SmemLayout::dout + kHalfTile, &tmap_do, &bars->do_full, 64, row0, hq);
       }
+      float* lse2 = vecs + st * 256;
+      float* dvec = lse2 + 128;
+      *reinterpret_cast<float4*>(lse2 + lane * 4) = make_float4(l2[0], l2[1], l2[2], l2[3]);
+      *reinterpret_cast<float4*>(dvec + lane * 4) = make_float4(dd[0], dd[1], dd[2], dd[3]);
       __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->vec_full[st]);
     }
   } else if (warp == 12) {
     // ===================== MMA issuer =====================
@@ -303,6 +321,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&bars->dq_drained);
       BWD_TRACE(warp == 0 && lane == 0, it, 10);
+#ifdef DA_BWD_DQ_TMA
+      // stage [32 q][32 d] boxes (this warp's 32 head-dim columns) and let TMA
+      // reduce them into dq_acc: no LSU atomics; OOB query rows are clipped
+      float* box = reinterpret_cast<float*>(smem + SmemLayout::dq_stage) + warp * 32 * 32;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 32; ++k) box[k * 32 + lane] = p.scale * __uint_as_float(r[c][k]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_reduce_add_3d(&tmap_dq, box, warp * 32, row0 + c * 32, hq);
+          bulk_commit();
+        }
+      }
+#else
       // a warp reduces 32 consecutive floats of one dQ row per instruction (128 B)
       float* base = p.dq_acc + (static_cast<size_t>(hq) * p.rows_q + row0) * kHD + dcol;
       const int q_valid = min(kBM, p.rows_q - row0);
@@ -320,8 +356,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (c * 32 + k < q_valid)
               red_add_f32(base + static_cast<size_t>(c * 32 + k) * kHD, p.scale * __uint_as_float(r[c][k]));
       }
+#endif
       BWD_TRACE(warp == 0 && lane == 0, it, 11);
     }
+#ifdef DA_BWD_DQ_TMA
+    if (lane == 0) bulk_wait<0>();
+#endif
   } else {
     // ===================== compute (warps 4-11) =====================
     setmaxnreg_inc<136>();
@@ -340,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool diag = (p.mask == DA_MASK_DIAGONAL) && (it_qtile(it) == jt);
       const float* lse2 = vecs + st * 256 + half * 64;
       const float* dvec = vecs + st * 256 + 128 + half * 64;
-      mbar_wait(&bars->q_full[st], (it >> 1) & 1);  // lse/D rows visible
+      mbar_wait(&bars->vec_full[st], (it >> 1) & 1);  // lse/D rows visible
 
       // ---- phase A: P = exp2(S * scale*log2e - lse2)
       mbar_wait(&bars->s_full, it & 1);
@@ -466,7 +506,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 }  // namespace bwd
 
 cudaError_t launch_attn_bwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                            const CUtensorMap& tdo, const BwdParams& p, cudaStream_t stream) {
+                            const CUtensorMap& tdo, const CUtensorMap& tdq, const BwdParams& p,
+                            cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(bwd::attn_bwd_kernel,
@@ -483,7 +524,7 @@ cudaError_t launch_attn_bwd(const CUtensorMap& tq, const CUtensorMap& tk, const 
   }
   const int n_kv_tiles = (p.rows_kv + bwd::kBN - 1) / bwd::kBN;
   dim3 grid(n_kv_tiles * p.h_kv);
-  bwd::attn_bwd_kernel<<<grid, bwd::kThreads, bwd::kSmemBytes, stream>>>(tq, tk, tv, tdo, p);
+  bwd::attn_bwd_kernel<<<grid, bwd::kThreads, bwd::kSmemBytes, stream>>>(tq, tk, tv, tdo, tdq, p);
   return cudaGetLastError();
 }
 

@@ -63,6 +63,21 @@ da_status make_tmap_3d(CUtensorMap* map, const void* base, int64_t heads, int64_
   return DA_OK;
 }
 
+da_status make_tmap_f32_acc(CUtensorMap* map, void* base, int64_t heads, int64_t rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (fn == nullptr) return set_error(DA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {128, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(heads)};
+  const cuuint64_t strides[2] = {128 * 4, static_cast<cuuint64_t>(rows) * 128 * 4};
+  const cuuint32_t box[3] = {32, 32, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(DA_ERR_CUDA, "cuTensorMapEncodeTiled(f32) failed (" + std::to_string(r) + ")");
+  return DA_OK;
+}
+
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 unsigned long long* g_bwd_trace = nullptr;
@@ -231,12 +246,13 @@ da_status da_attn_bwd_chunk(const da_bwd_args* a, void* stream) {
     }
     return e == cudaSuccess ? DA_OK : da::cuda_error(e, "block_attn_backward(empty)");
   }
-  CUtensorMap tq, tk, tv, tdo;
+  CUtensorMap tq, tk, tv, tdo, tdq;
   da_status s;
   if ((s = da::make_tmap_3d(&tq, a->q, a->h_q, a->rows_q)) != DA_OK) return s;
   if ((s = da::make_tmap_3d(&tk, a->k, a->h_kv, a->rows_kv)) != DA_OK) return s;
   if ((s = da::make_tmap_3d(&tv, a->v, a->h_kv, a->rows_kv)) != DA_OK) return s;
   if ((s = da::make_tmap_3d(&tdo, a->d_out, a->h_q, a->rows_q)) != DA_OK) return s;
+  if ((s = da::make_tmap_f32_acc(&tdq, a->dq_acc, a->h_q, a->rows_q)) != DA_OK) return s;
   da::BwdParams p{};
   p.h_q = static_cast<int>(a->h_q);
   p.h_kv = static_cast<int>(a->h_kv);
@@ -252,7 +268,7 @@ da_status da_attn_bwd_chunk(const da_bwd_args* a, void* stream) {
   p.dk_acc = a->dk_acc;
   p.dv_acc = a->dv_acc;
   p.trace = da::g_bwd_trace;
-  cudaError_t e = da::launch_attn_bwd(tq, tk, tv, tdo, p, st);
+  cudaError_t e = da::launch_attn_bwd(tq, tk, tv, tdo, tdq, p, st);
   return e == cudaSuccess ? DA_OK : da::cuda_error(e, "da_attn_bwd_chunk launch");
 }
 

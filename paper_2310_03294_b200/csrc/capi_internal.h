@@ -13,5 +13,7 @@ da_status set_error(da_status s, const std::string& msg);
 da_status cuda_error(cudaError_t e, const char* where);
 const char* last_error();
 da_status make_tmap_3d(CUtensorMap* map, const void* base, int64_t heads, int64_t rows);
+// fp32 [heads][rows][128] accumulator, box {32, 32, 1}, no swizzle (dQ reduction)
+da_status make_tmap_f32_acc(CUtensorMap* map, void* base, int64_t heads, int64_t rows);
 cudaError_t launch_fill(float* dst, float value, int64_t n, cudaStream_t stream);
 }  // namespace da

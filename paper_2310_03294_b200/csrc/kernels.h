@@ -44,7 +44,8 @@ cudaError_t launch_attn_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const 
                             const FwdParams& p, cudaStream_t stream);
 
 cudaError_t launch_attn_bwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                            const CUtensorMap& tdo, const BwdParams& p, cudaStream_t stream);
+                            const CUtensorMap& tdo, const CUtensorMap& tdq, const BwdParams& p,
+                            cudaStream_t stream);
 
 cudaError_t launch_merge(const float* o_a, const float* m_a, const float* l_a, const float* o_b,
                          const float* m_b, const float* l_b, float* o_out, float* m_out,
