@@ -154,7 +154,17 @@ da_status da_convert_f32_bf16(const float* src, void* dst, int64_t n, void* stre
  *     kind: 0 KV, 1 Q, 2 PartialResult, 3 GradKV (PayloadKind order).
  * Call once with NULL buffers to size them (counts are always written).
  * ------------------------------------------------------------------------ */
-typedef enum da_schedule_kind { DA_SCHEDULE_RING = 0, DA_SCHEDULE_BALANCED = 1 } da_schedule_kind;
+typedef enum da_schedule_kind {
+  DA_SCHEDULE_RING = 0,         /* build_ring_schedule       schedule.cpp:60-77 */
+  DA_SCHEDULE_BALANCED = 1,     /* build_balanced_schedule   schedule.cpp:79-108 */
+  /* Backward schedules. The reference's backward is ring-only
+   * (BackwardMode::Vanilla, runtime.hpp:110); RING_BWD makes its order explicit
+   * (runtime.cpp:605-651), BALANCED_BWD is the load-balanced extension (SURVEY
+   * §8(f)1): the forward task table with KV/GradKV for direct pairs,
+   * Q = (q, dO, lse, D) bundle to the helper and Partial = dq contribution back. */
+  DA_SCHEDULE_RING_BWD = 2,
+  DA_SCHEDULE_BALANCED_BWD = 3
+} da_schedule_kind;
 
 da_status da_schedule_build(int workers, int kind, int32_t* steps_out, int32_t* tasks,
                             int64_t* n_tasks, int32_t* messages, int64_t* n_messages);
@@ -164,6 +174,12 @@ da_status da_schedule_build(int workers, int kind, int32_t* steps_out, int32_t* 
  * Negative on bad input. */
 int64_t da_schedule_validate(int workers, int32_t steps, const int32_t* tasks, int64_t n_tasks,
                              const int32_t* messages, int64_t n_messages);
+
+/* validate plus GradKV coverage for backward schedules (every direct pair
+ * returns its dk/dv to the kv owner no earlier than its step). */
+int64_t da_schedule_validate_backward(int workers, int32_t steps, const int32_t* tasks,
+                                      int64_t n_tasks, const int32_t* messages,
+                                      int64_t n_messages);
 
 /* ------------------------------------------------------------------------
  * Runtime (runtime.cpp:491-529, 720-750), P logical workers on ONE device —
@@ -198,6 +214,11 @@ typedef struct da_counters {
 da_status da_run_forward(const da_shards* shards, int schedule_kind, da_counters* counters,
                          void* stream);
 da_status da_run_backward(const da_shards* shards, da_counters* counters, void* stream);
+/* run_backward with an explicit backward schedule (DA_SCHEDULE_RING_BWD is
+ * identical to da_run_backward; DA_SCHEDULE_BALANCED_BWD balances the causal
+ * pairs like the forward). */
+da_status da_run_backward_sched(const da_shards* shards, int schedule_kind, da_counters* counters,
+                                void* stream);
 /* Frees the cached runtime workspace of the calling thread. */
 void da_runtime_release(void);
 
@@ -212,6 +233,8 @@ da_status da_rng_uniform(uint64_t state, int64_t n, double lo, double hi, int dt
 /* Debug: device buffer (64 x 16 uint64) receiving the backward kernel's
  * per-iteration clock64 timeline of CTA 0 in DA_TRACE builds; NULL disables. */
 void da_debug_set_bwd_trace(void* buf);
+/* Debug: same for the forward kernel (64 x 16 uint64). */
+void da_debug_set_fwd_trace(void* buf);
 
 /* Debug: compute the raw score block S = q kᵀ (fp32, unscaled) of the first
  * 128x128 tile of head 0 through the forward kernel's MMA path. */

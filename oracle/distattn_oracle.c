@@ -518,3 +518,151 @@ int dao_run_backward(int P, int64_t n, int64_t d, const double* q, const double*
   free(gq); free(gk); free(gv); free(pk); free(pv);
   return 0;
 }
+
+/* ---------------- backward over a schedule table (extension) ---------------- */
+int dao_run_backward_sched(int P, int kind, int64_t n, int64_t d, const double* q,
+                           const double* k, const double* v, const double* out,
+                           const double* lse, const double* d_out, double* dq, double* dk,
+                           double* dv, int64_t* counters) {
+  if (P < 1 || n % P != 0) return 2;
+  const int64_t rows = n / P;
+  const size_t osz = (size_t)(rows * d);
+  const double scale = 1.0 / sqrt((double)d);
+  int32_t steps = 0;
+  int64_t nt = 0, nm = 0;
+  dao_schedule_build(P, kind, &steps, NULL, &nt, NULL, &nm);
+  int32_t* tasks = (int32_t*)malloc(sizeof(int32_t) * 6 * (size_t)nt);
+  int32_t* msgs = (int32_t*)malloc(sizeof(int32_t) * 4 * (size_t)(nm + 1));
+  dao_schedule_build(P, kind, &steps, tasks, &nt, msgs, &nm);
+  memset(dq, 0, sizeof(double) * (size_t)(n * d));
+  memset(dk, 0, sizeof(double) * (size_t)(n * d));
+  memset(dv, 0, sizeof(double) * (size_t)(n * d));
+  double* gq = (double*)malloc(sizeof(double) * osz);
+  double* gk = (double*)malloc(sizeof(double) * osz);
+  double* gv = (double*)malloc(sizeof(double) * osz);
+  /* pending GradKV indexed by sender, pending dq partial indexed by helper */
+  double* pk = (double*)malloc(sizeof(double) * osz * (size_t)P);
+  double* pv = (double*)malloc(sizeof(double) * osz * (size_t)P);
+  double* pq = (double*)malloc(sizeof(double) * osz * (size_t)P);
+  int* gk_to = (int*)malloc(sizeof(int) * (size_t)P); /* receiver of sender's GradKV, 0 = none */
+  int64_t c[10] = {0};
+  for (int t = 0; t < steps; ++t) {
+    for (int w = 0; w < P; ++w) gk_to[w] = 0;
+    for (int64_t i = 0; i < nt; ++i) {
+      const int32_t* tk = tasks + 6 * i;
+      if (tk[0] != t || tk[1] == 3 || tk[1] == 2) continue;
+      const int w = tk[2];
+      const size_t wo = (size_t)(w - 1) * osz;
+      ++c[8];
+      if (tk[1] == 0) {
+        dao_block_attn_backward(q + wo, rows, k + wo, v + wo, rows, d, out + wo,
+                                lse + (w - 1) * rows, d_out + wo, 0, scale, 16, 16, gq, gk, gv);
+        for (size_t x = 0; x < osz; ++x) {
+          dq[wo + x] += gq[x];
+          dk[wo + x] += gk[x];
+          dv[wo + x] += gv[x];
+        }
+      } else if (tk[2] == tk[3]) { /* direct */
+        const int r = tk[4];
+        const size_t ro = (size_t)(r - 1) * osz;
+        count_msg(c, 0, rows, d);
+        c[9] = 1;
+        dao_block_attn_backward(q + wo, rows, k + ro, v + ro, rows, d, out + wo,
+                                lse + (w - 1) * rows, d_out + wo, 1, scale, 16, 16, gq, pk + wo,
+                                pv + wo);
+        gk_to[w - 1] = r;
+        for (size_t x = 0; x < osz; ++x) dq[wo + x] += gq[x];
+      } else { /* helper w for owner o on its own kv */
+        const int o = tk[3];
+        const size_t oo = (size_t)(o - 1) * osz;
+        c[1] += rows * (2 * d + 2);
+        ++c[5];
+        c[9] = 1;
+        dao_block_attn_backward(q + oo, rows, k + wo, v + wo, rows, d, out + oo,
+                                lse + (o - 1) * rows, d_out + oo, 1, scale, 16, 16, pq + wo, gk,
+                                gv);
+        for (size_t x = 0; x < osz; ++x) {
+          dk[wo + x] += gk[x];
+          dv[wo + x] += gv[x];
+        }
+      }
+    }
+    /* GradKV folds in ascending receiver order (runtime.cpp:636-649) */
+    for (int r = 1; r <= P; ++r)
+      for (int s = 1; s <= P; ++s)
+        if (gk_to[s - 1] == r) {
+          count_msg(c, 3, rows, d);
+          const size_t ro = (size_t)(r - 1) * osz, so = (size_t)(s - 1) * osz;
+          for (size_t x = 0; x < osz; ++x) {
+            dk[ro + x] += pk[so + x];
+            dv[ro + x] += pv[so + x];
+          }
+        }
+    /* dq partial folds in merge order */
+    for (int64_t i = 0; i < nt; ++i) {
+      const int32_t* tk = tasks + 6 * i;
+      if (tk[0] != t || tk[1] != 2) continue;
+      const int o = tk[2], h = tk[5];
+      c[2] += rows * d;
+      ++c[6];
+      const size_t oo = (size_t)(o - 1) * osz, ho = (size_t)(h - 1) * osz;
+      for (size_t x = 0; x < osz; ++x) dq[oo + x] += pq[ho + x];
+    }
+  }
+  if (counters) memcpy(counters, c, sizeof(c));
+  free(tasks); free(msgs); free(gq); free(gk); free(gv); free(pk); free(pv); free(pq); free(gk_to);
+  return 0;
+}
+
+/* block_attn_backward with D = rowsum(dO * O) supplied by the caller (the
+ * value backward_aux computes, flashcore.hpp:250-261): bit-identical to
+ * dao_block_attn_backward when d_vec came from dao_backward_aux. */
+int dao_block_attn_backward_with_d(const double* q, int64_t rq, const double* k, const double* v,
+                                   int64_t rk, int64_t d, const double* d_vec, const double* lse,
+                                   const double* d_out, int mask, double scale, int64_t br0,
+                                   int64_t bc0, double* dq, double* dk, double* dv) {
+  /* out is only used to form D: pass a fake O = d_vec spread so that
+   * rowsum(dO * O) reproduces d_vec is not possible in general, so restate. */
+  if (br0 <= 0 || bc0 <= 0) return 2;
+  if (mask == 0 && rq != rk) return 1;
+  memset(dq, 0, sizeof(double) * (size_t)(rq * d));
+  memset(dk, 0, sizeof(double) * (size_t)(rk * d));
+  memset(dv, 0, sizeof(double) * (size_t)(rk * d));
+  if (mask == 2) return 0;
+  double* p = (double*)malloc(sizeof(double) * (size_t)(br0 * bc0));
+  for (int64_t j0 = 0; j0 < rk; j0 += bc0) {
+    const int64_t bc = bc0 < rk - j0 ? bc0 : rk - j0;
+    for (int64_t i0 = 0; i0 < rq; i0 += br0) {
+      const int64_t br = br0 < rq - i0 ? br0 : rq - i0;
+      if (mask == 0 && j0 > i0 + br - 1) continue;
+      for (int64_t r = 0; r < br; ++r)
+        for (int64_t c = 0; c < bc; ++c) {
+          if (mask == 0 && j0 + c > i0 + r) {
+            p[r * bc + c] = 0.0;
+            continue;
+          }
+          double dot = 0.0;
+          for (int64_t x = 0; x < d; ++x) dot += q[(i0 + r) * d + x] * k[(j0 + c) * d + x];
+          p[r * bc + c] = exp(dot * scale - lse[i0 + r]);
+        }
+      for (int64_t r = 0; r < br; ++r)
+        for (int64_t c = 0; c < bc; ++c) {
+          const double pv = p[r * bc + c];
+          for (int64_t x = 0; x < d; ++x) dv[(j0 + c) * d + x] += pv * d_out[(i0 + r) * d + x];
+          double dp = 0.0;
+          for (int64_t x = 0; x < d; ++x) dp += d_out[(i0 + r) * d + x] * v[(j0 + c) * d + x];
+          p[r * bc + c] = pv * (dp - d_vec[i0 + r]);
+        }
+      for (int64_t r = 0; r < br; ++r)
+        for (int64_t c = 0; c < bc; ++c) {
+          const double sp = scale * p[r * bc + c];
+          for (int64_t x = 0; x < d; ++x) {
+            dq[(i0 + r) * d + x] += sp * k[(j0 + c) * d + x];
+            dk[(j0 + c) * d + x] += sp * q[(i0 + r) * d + x];
+          }
+        }
+    }
+  }
+  free(p);
+  return 0;
+}

@@ -79,6 +79,24 @@ int dao_run_backward(int workers, int64_t n, int64_t d, const double* q, const d
                      const double* v, const double* out, const double* lse, const double* d_out,
                      double* dq, double* dk, double* dv, int64_t* counters10);
 
+/* block_attn_backward with a caller-supplied D (from dao_backward_aux). */
+int dao_block_attn_backward_with_d(const double* q, int64_t rq, const double* k, const double* v,
+                                   int64_t rk, int64_t d, const double* d_vec, const double* lse,
+                                   const double* d_out, int mask, double scale, int64_t block_rows,
+                                   int64_t block_cols, double* dq, double* dk, double* dv);
+
+/* Backward over an explicit schedule table (kind 0 ring, 1 balanced):
+ * EXTENSION, the reference has only the ring order. Local/direct tasks follow
+ * runtime.cpp:605-651 (dq += immediately, GradKV folded at the end of the step
+ * in ascending receiver order); a helper h for owner o computes the pair
+ * (o, h), adds dk/dv to its own chunk immediately and returns dq, which the
+ * owner folds at the end of the step in merge order. Ring reproduces
+ * dao_run_backward bit-exactly. */
+int dao_run_backward_sched(int workers, int kind, int64_t n, int64_t d, const double* q,
+                           const double* k, const double* v, const double* out,
+                           const double* lse, const double* d_out, double* dq, double* dk,
+                           double* dv, int64_t* counters10);
+
 #ifdef __cplusplus
 }
 #endif

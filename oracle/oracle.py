@@ -61,6 +61,11 @@ def lib():
                                       _i64p]
         L.dao_run_backward.argtypes = [C.c_int, C.c_int64, C.c_int64, _d, _d, _d, _d, _d, _d, _d,
                                        _d, _d, _i64p]
+        L.dao_block_attn_backward_with_d.argtypes = [_d, C.c_int64, _d, _d, C.c_int64, C.c_int64,
+                                                     _d, _d, _d, C.c_int, C.c_double, C.c_int64,
+                                                     C.c_int64, _d, _d, _d]
+        L.dao_run_backward_sched.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, _d, _d, _d,
+                                             _d, _d, _d, _d, _d, _d, _i64p]
         L.dao_rng_next_u64.argtypes = [C.POINTER(C.c_uint64)]
         L.dao_rng_next_u64.restype = C.c_uint64
         L.dao_rng_next_unit.argtypes = [C.POINTER(C.c_uint64)]
@@ -165,6 +170,24 @@ def block_attn_backward(q, k, v, out, lse, d_out, mask: str, scale: float, block
     return dq, dk, dv
 
 
+def backward_aux(d_out, out):
+    d_out, out = (np.ascontiguousarray(x, dtype=np.float64) for x in (d_out, out))
+    dv = np.empty(out.shape[0])
+    lib().dao_backward_aux(d_out, out, out.shape[0], out.shape[1], dv)
+    return dv
+
+
+def block_attn_backward_with_d(q, k, v, d_vec, lse, d_out, mask: str, scale: float,
+                               blocks=(16, 16)):
+    q, k, v, d_vec, lse, d_out = (np.ascontiguousarray(x, dtype=np.float64)
+                                  for x in (q, k, v, d_vec, lse, d_out))
+    dq, dk, dv = np.empty_like(q), np.empty_like(k), np.empty_like(v)
+    _ok(lib().dao_block_attn_backward_with_d(q, q.shape[0], k, v, k.shape[0], q.shape[1], d_vec,
+                                             lse, d_out, MASK[mask], scale, blocks[0], blocks[1],
+                                             dq, dk, dv), "block_attn_backward_with_d")
+    return dq, dk, dv
+
+
 def dense_oracle(q, k, v, causal: bool, scale: float):
     q, k, v = (np.ascontiguousarray(x, dtype=np.float64) for x in (q, k, v))
     out, lse = np.empty((q.shape[0], v.shape[1])), np.empty(q.shape[0])
@@ -201,6 +224,18 @@ def run_backward(q, k, v, out, lse, d_out, workers: int):
     c = (C.c_int64 * 10)()
     _ok(lib().dao_run_backward(workers, n, d, q, k, v, out, lse, d_out, dq, dk, dv, c),
         "run_backward")
+    return dq, dk, dv, list(c)
+
+
+def run_backward_sched(q, k, v, out, lse, d_out, workers: int, schedule: str):
+    """Backward over the ring or balanced backward schedule (balanced: extension)."""
+    q, k, v, out, lse, d_out = (np.ascontiguousarray(x, dtype=np.float64)
+                                for x in (q, k, v, out, lse, d_out))
+    n, d = q.shape
+    dq, dk, dv = np.empty((n, d)), np.empty((n, d)), np.empty((n, d))
+    c = (C.c_int64 * 10)()
+    _ok(lib().dao_run_backward_sched(workers, 0 if schedule == "ring" else 1, n, d, q, k, v, out,
+                                     lse, d_out, dq, dk, dv, c), "run_backward_sched")
     return dq, dk, dv, list(c)
 
 

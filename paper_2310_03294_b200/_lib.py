@@ -63,11 +63,15 @@ SIGNATURES = {
     "da_schedule_build": (C.c_int, [C.c_int, C.c_int, C.POINTER(i32), C.POINTER(i32),
                                     C.POINTER(i64), C.POINTER(i32), C.POINTER(i64)]),
     "da_schedule_validate": (i64, [C.c_int, i32, C.POINTER(i32), i64, C.POINTER(i32), i64]),
+    "da_schedule_validate_backward": (i64, [C.c_int, i32, C.POINTER(i32), i64, C.POINTER(i32),
+                                            i64]),
     "da_run_forward": (C.c_int, [C.POINTER(Shards), C.c_int, C.POINTER(Counters), vp]),
+    "da_run_backward_sched": (C.c_int, [C.POINTER(Shards), C.c_int, C.POINTER(Counters), vp]),
     "da_run_backward": (C.c_int, [C.POINTER(Shards), C.POINTER(Counters), vp]),
     "da_runtime_release": (None, []),
     "da_rng_uniform": (C.c_int, [C.c_uint64, i64, C.c_double, C.c_double, C.c_int, vp, vp]),
     "da_debug_set_bwd_trace": (None, [vp]),
+    "da_debug_set_fwd_trace": (None, [vp]),
     "da_debug_scores": (C.c_int, [vp, vp, i64, vp, vp]),
 }
 

@@ -424,6 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld_32x32b_x32(dp_tmem, dr[0]);
       tmem_ld_32x32b_x32(dp_tmem + 32, dr[1]);
       tmem_ld_wait();
+      BWD_TRACE(cw == 0 && lane == 0, it, 12);
       uint32_t dsk[32];
 #pragma unroll
       for (int c = 0; c < 64; c += 4) {
@@ -436,6 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         dsk[c / 2] = pack_bf16x2(s0, s1);
         dsk[c / 2 + 1] = pack_bf16x2(s2, s3);
       }
+      BWD_TRACE(cw == 0 && lane == 0, it, 13);
       // dS^T (bf16) -> TMEM (A operand of dK) and -> smem (B operand of dQ^T)
       tmem_st_32x32b_x32(dp_tmem, dsk);
 #pragma unroll
@@ -444,8 +446,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         *reinterpret_cast<uint4*>(ds_smem + phys * 16) =
             make_uint4(dsk[4 * ch + 0], dsk[4 * ch + 1], dsk[4 * ch + 2], dsk[4 * ch + 3]);
       }
+      BWD_TRACE(cw == 0 && lane == 0, it, 14);
       fence_proxy_async_smem();
       tmem_st_wait();
+      BWD_TRACE(cw == 0 && lane == 0, it, 15);
       tc_fence_before();
       mbar_arrive(&bars->ds_full);
       BWD_TRACE(cw == 0 && lane == 0, it, 8);

@@ -24,6 +24,18 @@
 namespace da {
 namespace fwd {
 
+#ifdef DA_TRACE
+#define FWD_TRACE(cond, j, slot)                                                \
+  do {                                                                          \
+    if ((cond) && p.trace != nullptr && blockIdx.x == 0 && (j) < 64)            \
+      p.trace[(j) * 16 + (slot)] = clock64();                                   \
+  } while (0)
+#else
+#define FWD_TRACE(cond, j, slot) \
+  do {                           \
+  } while (0)
+#endif
+
 constexpr int kBM = 128;
 constexpr int kBN = 128;
 constexpr int kHD = 128;
@@ -199,12 +211,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool has_next = j + 1 < nmax;
         const int s1 = (j + 1) % kStages;
         const uint32_t ph1 = ((j + 1) / kStages) & 1;
+        FWD_TRACE(true, j, 0);
         mbar_wait(&bars->v_full[s], ph);
+        FWD_TRACE(true, j, 7);
         if (has_next) mbar_wait(&bars->k_full[s1], ph1);
+        FWD_TRACE(true, j, 8);
         tc_fence_after();
         for (int t = 0; t < 2; ++t) {
           if (j < n_t[t]) {
             mbar_wait(&bars->p_full[t], j & 1);
+            FWD_TRACE(true, j, 1 + t);
             tc_fence_after();
             issue_pv(t, s, j > 0);
             mma_commit(&bars->o_done[t]);
@@ -237,6 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     for (int j = 0; j < n_tiles; ++j) {
       mbar_wait(&bars->s_full[t], j & 1);
+      FWD_TRACE(quarter == 0 && lane == 0, j, 3 + 2 * t);
       tc_fence_after();
       uint32_t sr[4][32];
 #pragma unroll
@@ -332,6 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&bars->p_full[t]);
+      FWD_TRACE(quarter == 0 && lane == 0, j, 4 + 2 * t);
     }
 
     // ===================== epilogue =====================

@@ -81,6 +81,7 @@ da_status make_tmap_f32_acc(CUtensorMap* map, void* base, int64_t heads, int64_t
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 unsigned long long* g_bwd_trace = nullptr;
+unsigned long long* g_fwd_trace = nullptr;
 
 }  // namespace da
 
@@ -176,6 +177,7 @@ da_status da_attn_fwd_chunk(const da_fwd_args* a, void* stream) {
   p.lse_out = a->lse_out;
   p.degenerate_flag = a->degenerate_flag;
   p.debug_s = nullptr;
+  p.trace = da::g_fwd_trace;
   cudaError_t e = da::launch_attn_fwd(tq, tk, tv, p, st);
   return e == cudaSuccess ? DA_OK : da::cuda_error(e, "da_attn_fwd_chunk launch");
 }
@@ -280,6 +282,7 @@ da_status da_convert_f32_bf16(const float* src, void* dst, int64_t n, void* stre
 
 // Debug (DA_TRACE builds only record): device buffer of 64*16 uint64 stamps.
 void da_debug_set_bwd_trace(void* buf) { da::g_bwd_trace = static_cast<unsigned long long*>(buf); }
+void da_debug_set_fwd_trace(void* buf) { da::g_fwd_trace = static_cast<unsigned long long*>(buf); }
 
 da_status da_debug_scores(const void* q, const void* k, int64_t rows, float* s_out, void* stream) {
   CUtensorMap tq, tk;

@@ -24,6 +24,7 @@ struct FwdParams {
   float* lse_out;
   int* degenerate_flag;
   float* debug_s;  // optional raw-score dump of tile (0,0) of head 0
+  unsigned long long* trace;  // DA_TRACE builds: per-iteration clock64 stamps of CTA 0
 };
 
 struct BwdParams {

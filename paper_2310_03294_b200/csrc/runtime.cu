@@ -226,9 +226,29 @@ da_status da_run_forward(const da_shards* s, int schedule_kind, da_counters* cou
 }
 
 da_status da_run_backward(const da_shards* s, da_counters* counters, void* stream) {
+  return da_run_backward_sched(s, DA_SCHEDULE_RING_BWD, counters, stream);
+}
+
+// Backward over a ring or balanced backward schedule. Every pair (q chunk p,
+// kv chunk r) is one block_attn_backward launch; dq goes to p's accumulator,
+// dk/dv to r's (zero-copy GradKV / local for helpers). Ring order reproduces
+// runtime.cpp:605-651; balanced order follows make_balanced_backward.
+da_status da_run_backward_sched(const da_shards* s, int schedule_kind, da_counters* counters,
+                                void* stream) {
   da_status rc = check_shards(s, true);
   if (rc != DA_OK) return rc;
   const int P = s->workers;
+  FlatSchedule sch;
+  if (schedule_kind == DA_SCHEDULE_RING_BWD || schedule_kind == DA_SCHEDULE_RING)
+    sch = make_ring_backward(P);
+  else if (schedule_kind == DA_SCHEDULE_BALANCED_BWD || schedule_kind == DA_SCHEDULE_BALANCED)
+    sch = make_balanced_backward(P);
+  else
+    return set_error(DA_ERR_CONFIG, "unknown schedule kind");
+  const auto errs = validate_backward_flat(sch);
+  if (!errs.empty())
+    return set_error(DA_ERR_SCHEDULE, "invalid schedule: " + errs.front() + " (" +
+                                          std::to_string(errs.size()) + " violations)");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e = g_ws.ensure(P, s->h_q, s->rows);
   if (e != cudaSuccess) return cuda_error(e, "run_backward workspace");
@@ -257,7 +277,6 @@ da_status da_run_backward(const da_shards* s, da_counters* counters, void* strea
     a.rows_kv = s->rows;
     a.d = s->d;
     a.dq_acc = s->dq[qw - 1];
-    // GradKV: the contribution folds straight into the kv owner's buffers
     a.dk_acc = s->dk[kvw - 1];
     a.dv_acc = s->dv[kvw - 1];
     a.accumulate_kv = 1;
@@ -265,38 +284,53 @@ da_status da_run_backward(const da_shards* s, da_counters* counters, void* strea
     a.mask = mask;
     return da_attn_bwd_chunk(&a, st);
   };
-  // ring order (runtime.cpp:605-651): step 0 diagonal, then kv of p - t
-  for (int t = 0; t < P; ++t) {
-    for (int p = 1; p <= P; ++p) {
-      Tally& me = tally[p - 1];
-      if (t == 0) {
-        ++me.c.attention_kernel_calls;
-        rc = chunk(p, p, DA_MASK_DIAGONAL);
-      } else if (t < p) {
-        const int r = p - t;
-        count(me.c, kMsgKV, s->rows, s->d, s->h_kv);
+  const int64_t R = s->rows, D = s->d;
+  for (int t = 0; t < sch.steps; ++t) {
+    for (const Task& k : sch.tasks) {
+      if (k.step != t || k.kind == kIdle || k.kind == kMerge) continue;
+      const int w = k.worker;
+      Tally& me = tally[w - 1];
+      ++me.c.attention_kernel_calls;
+      if (k.kind == kLocal) {
+        rc = chunk(w, w, DA_MASK_DIAGONAL);
+      } else if (k.worker == k.query_owner) {  // direct: KV in, GradKV out
+        count(me.c, kMsgKV, R, D, s->h_kv);
         me.acquire();
-        ++me.c.attention_kernel_calls;
-        rc = chunk(p, r, DA_MASK_FULL);
+        rc = chunk(w, k.kv_owner, DA_MASK_FULL);
+        me.release();
+      } else {  // helper: (q, dO, lse, D) bundle in, dq partial out
+        me.acquire();
+        me.c.q_scalars += R * (2 * D + 2) * s->h_q;
+        ++me.c.q_messages;
+        rc = chunk(k.query_owner, w, DA_MASK_FULL);
         me.release();
       }
       if (rc != DA_OK) return rc;
     }
-    if (t >= 1) {
-      for (int r = 1; r <= P; ++r) {
-        if (r + t > P) continue;
-        Tally& me = tally[r - 1];
-        count(me.c, kMsgGradKV, s->rows, s->d, s->h_kv);
+    // GradKV folds (ascending kv owner as runtime.cpp:636-649) and dq partial
+    // folds (the schedule's merge order) — accounting only: the kernels above
+    // already accumulated into the owners' buffers.
+    for (const Message& m : sch.messages) {
+      if (m.step != t) continue;
+      if (m.kind == kMsgGradKV) {
+        Tally& me = tally[m.to - 1];
+        count(me.c, kMsgGradKV, R, D, s->h_kv);
         me.acquire();
         me.release();
+      } else if (m.kind == kMsgPartial) {
+        Tally& me = tally[m.to - 1];
+        me.c.partial_scalars += R * D * s->h_q;
+        ++me.c.partial_messages;
       }
     }
   }
   if (counters) {
     da_counters c{};
     for (const Tally& ty : tally) {
-      c.kv_scalars += ty.c.kv_scalars; c.grad_scalars += ty.c.grad_scalars;
-      c.kv_messages += ty.c.kv_messages; c.grad_messages += ty.c.grad_messages;
+      c.kv_scalars += ty.c.kv_scalars; c.q_scalars += ty.c.q_scalars;
+      c.partial_scalars += ty.c.partial_scalars; c.grad_scalars += ty.c.grad_scalars;
+      c.kv_messages += ty.c.kv_messages; c.q_messages += ty.c.q_messages;
+      c.partial_messages += ty.c.partial_messages; c.grad_messages += ty.c.grad_messages;
       c.attention_kernel_calls += ty.c.attention_kernel_calls;
       c.max_remote_chunks_held = ty.max_held > c.max_remote_chunks_held ? ty.max_held
                                                                          : c.max_remote_chunks_held;

@@ -184,6 +184,49 @@ std::vector<std::string> validate_flat(const FlatSchedule& s) {
   return errs;
 }
 
+static FlatSchedule with_grad_kv(FlatSchedule s) {
+  // a GradKV message follows every direct task, in task order
+  std::vector<Message> grads;
+  for (const Task& k : s.tasks)
+    if (k.kind == kRemote && k.worker == k.query_owner)
+      grads.push_back({k.step, k.worker, k.kv_owner, kMsgGradKV});
+  s.messages.insert(s.messages.end(), grads.begin(), grads.end());
+  return s;
+}
+
+FlatSchedule make_ring_backward(int P) { return with_grad_kv(make_ring(P)); }
+FlatSchedule make_balanced_backward(int P) { return with_grad_kv(make_balanced(P)); }
+
+std::vector<std::string> validate_backward_flat(const FlatSchedule& s) {
+  FlatSchedule fwd = s;
+  std::vector<Message> grads;
+  fwd.messages.clear();
+  for (const Message& m : s.messages) (m.kind == kMsgGradKV ? grads : fwd.messages).push_back(m);
+  std::vector<std::string> errs = validate_flat(fwd);
+  std::vector<bool> used(grads.size(), false);
+  for (const Task& k : s.tasks) {
+    if (!(k.kind == kRemote && k.worker == k.query_owner)) continue;
+    bool found = false;
+    for (size_t i = 0; i < grads.size() && !found; ++i) {
+      const Message& g = grads[i];
+      if (!used[i] && g.from == k.worker && g.to == k.kv_owner && g.step >= k.step) {
+        used[i] = true;
+        found = true;
+      }
+    }
+    if (!found)
+      errs.push_back("step " + std::to_string(k.step) + ": gradient of pair (q=" +
+                     std::to_string(k.query_owner) + ", kv=" + std::to_string(k.kv_owner) +
+                     ") is never returned to its kv owner");
+  }
+  for (size_t i = 0; i < grads.size(); ++i)
+    if (!used[i])
+      errs.push_back("message (step=" + std::to_string(grads[i].step) + ", " +
+                     std::to_string(grads[i].from) + "->" + std::to_string(grads[i].to) +
+                     ", grad_kv) is never consumed");
+  return errs;
+}
+
 }  // namespace da
 
 extern "C" {
@@ -194,10 +237,14 @@ da_status da_schedule_build(int workers, int kind, int32_t* steps_out, int32_t* 
     return da::set_error(DA_ERR_CONFIG, kind == DA_SCHEDULE_RING
                                             ? "ring schedule needs at least 1 worker"
                                             : "balanced schedule needs at least 1 worker");
-  if (kind != DA_SCHEDULE_RING && kind != DA_SCHEDULE_BALANCED)
-    return da::set_error(DA_ERR_CONFIG, "unknown schedule kind");
-  const da::FlatSchedule s = kind == DA_SCHEDULE_RING ? da::make_ring(workers)
-                                                      : da::make_balanced(workers);
+  da::FlatSchedule s;
+  switch (kind) {
+    case DA_SCHEDULE_RING: s = da::make_ring(workers); break;
+    case DA_SCHEDULE_BALANCED: s = da::make_balanced(workers); break;
+    case DA_SCHEDULE_RING_BWD: s = da::make_ring_backward(workers); break;
+    case DA_SCHEDULE_BALANCED_BWD: s = da::make_balanced_backward(workers); break;
+    default: return da::set_error(DA_ERR_CONFIG, "unknown schedule kind");
+  }
   if (steps_out) *steps_out = s.steps;
   if (tasks) {
     for (size_t i = 0; i < s.tasks.size(); ++i) {
@@ -219,8 +266,8 @@ da_status da_schedule_build(int workers, int kind, int32_t* steps_out, int32_t* 
   return DA_OK;
 }
 
-int64_t da_schedule_validate(int workers, int32_t steps, const int32_t* tasks, int64_t n_tasks,
-                             const int32_t* messages, int64_t n_messages) {
+static int64_t validate_impl(int workers, int32_t steps, const int32_t* tasks, int64_t n_tasks,
+                             const int32_t* messages, int64_t n_messages, bool backward) {
   if (n_tasks < 0 || n_messages < 0 || (n_tasks > 0 && !tasks) || (n_messages > 0 && !messages)) {
     da::set_error(DA_ERR_CONFIG, "da_schedule_validate: bad buffers");
     return -1;
@@ -236,13 +283,24 @@ int64_t da_schedule_validate(int workers, int32_t steps, const int32_t* tasks, i
     const int32_t* o = messages + 4 * i;
     s.messages.push_back({o[0], o[1], o[2], o[3]});
   }
-  const auto errs = da::validate_flat(s);
+  const auto errs = backward ? da::validate_backward_flat(s) : da::validate_flat(s);
   if (!errs.empty()) {
     std::string all;
     for (const auto& e : errs) all += (all.empty() ? "" : "\n") + e;
     da::set_error(DA_ERR_SCHEDULE, all);
   }
   return static_cast<int64_t>(errs.size());
+}
+
+int64_t da_schedule_validate(int workers, int32_t steps, const int32_t* tasks, int64_t n_tasks,
+                             const int32_t* messages, int64_t n_messages) {
+  return validate_impl(workers, steps, tasks, n_tasks, messages, n_messages, false);
+}
+
+int64_t da_schedule_validate_backward(int workers, int32_t steps, const int32_t* tasks,
+                                      int64_t n_tasks, const int32_t* messages,
+                                      int64_t n_messages) {
+  return validate_impl(workers, steps, tasks, n_tasks, messages, n_messages, true);
 }
 
 }  // extern "C"

@@ -32,4 +32,18 @@ FlatSchedule make_ring(int P);
 FlatSchedule make_balanced(int P);
 std::vector<std::string> validate_flat(const FlatSchedule& s);
 
+// Backward schedules (extension: the reference's backward is ring-only,
+// runtime.hpp:110). Task tables are the forward ones; message semantics:
+//   KV        kv owner -> direct worker           (k, v)
+//   GradKV    direct worker -> kv owner           (dk, dv contribution)
+//   Q         query owner -> helper               (q, dO, lse, D bundle)
+//   Partial   helper -> query owner               (dq contribution, folded by the
+//                                                  RescaleMerge task in helper order)
+// Ring backward = the reference run_backward order (runtime.cpp:605-651).
+FlatSchedule make_ring_backward(int P);
+FlatSchedule make_balanced_backward(int P);
+// validate_flat's invariants plus: every direct pair (p, r) returns a GradKV
+// p -> r no earlier than its step, and no other GradKV exists.
+std::vector<std::string> validate_backward_flat(const FlatSchedule& s);
+
 }  // namespace da

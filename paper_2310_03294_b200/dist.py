@@ -35,7 +35,9 @@ from dataclasses import dataclass
 import torch
 import torch.distributed as tdist
 
-from .schedule import TaskKind, build_balanced_schedule, build_ring_schedule, validate
+from .schedule import (TaskKind, build_balanced_backward_schedule, build_balanced_schedule,
+                       build_ring_backward_schedule, build_ring_schedule, validate,
+                       validate_backward)
 from .errors import ConfigError, ScheduleError, StateError
 
 
@@ -74,10 +76,11 @@ class CudaBackend:
     def bwd_aux(self, d_out, out):
         return self.F.backward_aux(d_out, out)
 
-    def grads(self, q, k, v, out, lse, d_out, d_vec, mask: str, dq, dk, dv, accumulate_kv: bool):
+    def grads(self, q, k, v, lse, d_out, d_vec, mask: str, dq, dk, dv, accumulate_kv: bool):
+        """dq += contribution; dk/dv += (accumulate_kv) or = contribution."""
         F = self.F
         mm = F.MaskMode.Diagonal if mask == "diagonal" else F.MaskMode.Full
-        F.block_attn_backward(q, k, v, out, lse, d_out, mm, d_vec=d_vec,
+        F.block_attn_backward(q, k, v, None, lse, d_out, mm, d_vec=d_vec,
                               grads=F.ChunkGrads(dq, dk, dv), accumulate_kv=accumulate_kv)
 
     def add_(self, dst, src):
@@ -162,6 +165,45 @@ def forward_plan(schedule, worker: int) -> list[StepPlan]:
                            if m.step == t and m.from_ == worker and int(m.kind) == 0)
         p.q_sends = tuple(m.to for m in schedule.messages
                           if m.step == t and m.from_ == worker and int(m.kind) == 1)
+        plans.append(p)
+    return plans
+
+
+@dataclass
+class BwdStepPlan:
+    action: str = "idle"     # idle | local | direct | help
+    peer: int = 0            # 1-based: kv owner (direct) or query owner (help)
+    kv_sends: tuple = ()     # destinations of my KV this step
+    q_sends: tuple = ()      # destinations of my (q, dO, lse, D) bundle
+    gradkv_from: tuple = ()  # senders of GradKV folded into my dk/dv this step
+    merges: tuple = ()       # helpers whose dq partial I fold this step, in order
+
+
+def backward_plan(schedule, worker: int) -> list[BwdStepPlan]:
+    plans = []
+    for t, step in enumerate(schedule.steps):
+        p = BwdStepPlan()
+        for task in step:
+            if task.worker != worker:
+                continue
+            if task.kind == TaskKind.LocalAttn:
+                p.action = "local"
+            elif task.kind == TaskKind.RemoteAttn:
+                if task.query_owner == worker:
+                    p.action, p.peer = "direct", task.kv_owner
+                else:
+                    p.action, p.peer = "help", task.query_owner
+            elif task.kind == TaskKind.RescaleMerge:
+                p.merges += (task.helper,)
+        for m in schedule.messages:
+            if m.step != t:
+                continue
+            if m.from_ == worker and int(m.kind) == 0:
+                p.kv_sends += (m.to,)
+            elif m.from_ == worker and int(m.kind) == 1:
+                p.q_sends += (m.to,)
+            elif m.to == worker and int(m.kind) == 3:
+                p.gradkv_from += (m.from_,)
         plans.append(p)
     return plans
 
@@ -279,8 +321,12 @@ class DistRuntime:
         self.saved = (q, k, v, out, lse)
         return out, lse
 
-    def backward(self, d_out, overlap: bool = True):
-        """Ring backward reusing the saved O and LSE (no forward recompute)."""
+    def backward(self, d_out, schedule: str = "ring", overlap: bool = True):
+        """Backward reusing the saved O and LSE (no forward recompute).
+
+        schedule="ring": the reference order (runtime.cpp:605-651);
+        schedule="balanced": the load-balanced extension (helpers compute the
+        wrap-around owners' pairs on their own kv and return dq)."""
         if self.saved is None:
             raise StateError("run_backward requires forward output and logsumexp")
         q, k, v, out, lse = self.saved
@@ -288,52 +334,90 @@ class DistRuntime:
         h, rows, d = q.shape
         hk = k.shape[0]
         be, tr = self.backend, self.transport
-        dq = self._buf("dq", (h, rows, d), be.grad_dtype)
-        dk = self._buf("dk", (hk, rows, d), be.grad_dtype)
-        dv = self._buf("dv", (hk, rows, d), be.grad_dtype)
-        dq.zero_()
+        sched = (build_balanced_backward_schedule(P) if schedule == "balanced"
+                 else build_ring_backward_schedule(P))
+        viol = validate_backward(sched)
+        if viol:
+            raise ScheduleError(f"invalid schedule: {viol[0]} ({len(viol)} violations)")
+        plans = backward_plan(sched, w)
+        gd = be.grad_dtype
+        dq = self._buf("dq", (h, rows, d), gd)
+        dk = self._buf("dk", (hk, rows, d), gd)
+        dv = self._buf("dv", (hk, rows, d), gd)
+        for t_ in (dq, dk, dv):
+            t_.zero_()
         d_vec = be.bwd_aux(d_out, out)
         kv_slot = [(self._buf(f"bk{i}", (hk, rows, d), k.dtype), self._buf(f"bv{i}", (hk, rows, d), v.dtype))
                    for i in range(2)]
-        g_send = [(self._buf(f"gk{i}", (hk, rows, d), be.grad_dtype),
-                   self._buf(f"gv{i}", (hk, rows, d), be.grad_dtype)) for i in range(2)]
-        g_recv = (self._buf("grk", (hk, rows, d), be.grad_dtype),
-                  self._buf("grv", (hk, rows, d), be.grad_dtype))
+        bundle = [(self._buf(f"bq{i}", (h, rows, d), q.dtype), self._buf(f"bdo{i}", (h, rows, d), d_out.dtype),
+                   self._buf(f"blse{i}", (h, rows), lse.dtype), self._buf(f"bD{i}", (h, rows), d_vec.dtype))
+                  for i in range(2)]
+        g_send = [(self._buf(f"gk{i}", (hk, rows, d), gd), self._buf(f"gv{i}", (hk, rows, d), gd))
+                  for i in range(2)]
+        q_send = [self._buf(f"gq{i}", (h, rows, d), gd) for i in range(2)]
+        g_recv = (self._buf("grk", (hk, rows, d), gd), self._buf("grv", (hk, rows, d), gd))
 
-        def post_kv(t):
-            """step t >= 1: I send my KV to w + t; I receive KV of w - t."""
+        def post_operands(t):
+            p = plans[t]
             sends, recvs = [], []
-            if w + t <= P:
-                sends += [(k, w + t - 1), (v, w + t - 1)]
+            for dst in p.kv_sends:
+                sends += [(k, dst - 1), (v, dst - 1)]
                 self._sent(k, v)
-            if w - t >= 1:
+            for dst in p.q_sends:
+                sends += [(q, dst - 1), (d_out, dst - 1), (lse, dst - 1), (d_vec, dst - 1)]
+                self._sent(q, d_out, lse, d_vec)
+            if p.action == "direct":
                 ks, vs = kv_slot[t % 2]
-                recvs += [(ks, w - t - 1), (vs, w - t - 1)]
+                recvs += [(ks, p.peer - 1), (vs, p.peer - 1)]
+            elif p.action == "help":
+                recvs += [(x, p.peer - 1) for x in bundle[t % 2]]
             return tr.exchange(sends, recvs)
 
-        be.grads(q, k, v, out, lse, d_out, d_vec, "diagonal", dq, dk, dv, accumulate_kv=False)
-        pending = post_kv(1) if P > 1 else _Done()
-        for t in range(1, P):
+        held = 0
+        pending = post_operands(0) if P > 1 else _Done()
+        for t, p in enumerate(plans):
             handle = pending
-            nxt = post_kv(t + 1) if (overlap and t + 1 < P) else None
+            nxt = post_operands(t + 1) if (overlap and t + 1 < len(plans)) else None
             handle.wait()
-            gsend = None
-            if w - t >= 1:
+            held = max(held, (1 if p.action in ("direct", "help") else 0) +
+                       (1 if nxt is not None and plans[t + 1].action in ("direct", "help") else 0))
+            sends = []
+            if p.action == "local":
+                be.grads(q, k, v, lse, d_out, d_vec, "diagonal", dq, dk, dv, accumulate_kv=True)
+            elif p.action == "direct":
                 ks, vs = kv_slot[t % 2]
                 gk, gv = g_send[t % 2]
-                be.grads(q, ks, vs, out, lse, d_out, d_vec, "full", dq, gk, gv, accumulate_kv=False)
-                gsend = [(gk, w - t - 1), (gv, w - t - 1)]
+                be.grads(q, ks, vs, lse, d_out, d_vec, "full", dq, gk, gv, accumulate_kv=False)
+                sends += [(gk, p.peer - 1), (gv, p.peer - 1)]
                 self._sent(gk, gv)
-            grecv = [(g_recv[0], w + t - 1), (g_recv[1], w + t - 1)] if w + t <= P else []
-            # GradKV leaves right after its kernel; waiting also retires the send
-            # buffer before it is rewritten two steps later
-            tr.exchange(gsend or [], grecv).wait()
-            if grecv:
+            elif p.action == "help":
+                bq, bdo, blse, bD = bundle[t % 2]
+                gq = q_send[t % 2]
+                gq.zero_()
+                be.grads(bq, k, v, blse, bdo, bD, "full", gq, dk, dv, accumulate_kv=True)
+                sends.append((gq, p.peer - 1))
+                self._sent(gq)
+            recvs = [(g_recv[0], s - 1) for s in p.gradkv_from[:1]] + \
+                    [(g_recv[1], s - 1) for s in p.gradkv_from[:1]]
+            part_bufs = []
+            for hw in p.merges:
+                buf = self._buf(f"gqr{hw}", (h, rows, d), gd)
+                part_bufs.append(buf)
+                recvs.append((buf, hw - 1))
+            if len(p.gradkv_from) > 1:
+                raise ScheduleError("at most one GradKV per worker and step is supported")
+            # results leave right after their kernels; waiting also retires the
+            # send buffers before they are rewritten two steps later
+            tr.exchange(sends, recvs).wait()
+            if p.gradkv_from:
                 be.add_(dk, g_recv[0])
                 be.add_(dv, g_recv[1])
-            if not overlap and t + 1 < P:
-                nxt = post_kv(t + 1)
+            for buf in part_bufs:
+                be.add_(dq, buf)
+            if not overlap and t + 1 < len(plans):
+                nxt = post_operands(t + 1)
             pending = nxt if nxt is not None else _Done()
+        self.trace["max_remote_chunks_held_bwd"] = held
         return dq, dk, dv
 
 
@@ -341,7 +425,7 @@ class DistRuntime:
 def bench_main(args) -> int:
     """torchrun entry for bench.py --gpus N: sequence-parallel fwd+bwd of the
     Llama-7B attention layer at seq 32K x N (32K tokens per GPU, weak scaling),
-    balanced forward + ring backward over NCCL."""
+    balanced forward + balanced backward over NCCL."""
     import json
     import statistics
     import time
@@ -361,7 +445,7 @@ def bench_main(args) -> int:
 
     def step():
         rt.forward(q, k, v, "balanced")
-        rt.backward(do)
+        rt.backward(do, "balanced")
 
     for _ in range(args.warmup):
         step()
@@ -384,7 +468,7 @@ def bench_main(args) -> int:
                 "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
                 "config": {"workload": f"llama7b-attn causal fwd+bwd, 32 heads, d=128, seq "
-                                       f"{n_total} over {world} B200 (balanced fwd, ring bwd, NCCL)",
+                                       f"{n_total} over {world} B200 (balanced fwd + bwd, NCCL)",
                            "heads": heads, "d": d, "seq_len": n_total, "tokens_per_gpu": rows},
                 "tokens_per_s": n_total / (ms * 1e-3),
                 "tflops_per_gpu": fl / (ms * 1e-3) / 1e12 / world}

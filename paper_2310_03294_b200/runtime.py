@@ -197,9 +197,12 @@ def run_forward(shards: list[SequenceShard], schedule: Schedule | str = "balance
     return _trace(len(shards), c)
 
 
-def run_backward(shards: list[SequenceShard], stream=None) -> ExecutionTrace:
-    """runtime.cpp:720-750 (ring order; BackwardMode::Vanilla). Requires
-    forward state and d_out; writes fp32 dq/dk/dv into the shards."""
+def run_backward(shards: list[SequenceShard], schedule: str = "ring",
+                 stream=None) -> ExecutionTrace:
+    """runtime.cpp:720-750. schedule="ring" is the reference order
+    (BackwardMode::Vanilla); "balanced" is the load-balanced backward
+    extension (schedule.build_balanced_backward_schedule). Requires forward
+    state and d_out; writes fp32 dq/dk/dv into the shards."""
     for s in shards:
         if not s.has_forward_state():
             raise StateError("run_backward requires forward output and logsumexp")
@@ -216,7 +219,9 @@ def run_backward(shards: list[SequenceShard], stream=None) -> ExecutionTrace:
     st, keep = _shards_struct(shards, True)
     c = _lib.Counters()
     strm = stream if stream is not None else torch.cuda.current_stream()
-    check(_lib.lib().da_run_backward(C.byref(st), C.byref(c), C.c_void_p(strm.cuda_stream)))
+    kind = {"ring": 2, "balanced": 3}[schedule]
+    check(_lib.lib().da_run_backward_sched(C.byref(st), kind, C.byref(c),
+                                           C.c_void_p(strm.cuda_stream)))
     del keep
     return _trace(len(shards), c)
 

@@ -117,13 +117,32 @@ def build_balanced_schedule(workers: int) -> Schedule:
     return _build(workers, 1)
 
 
-def validate(s: Schedule) -> list:
+def build_ring_backward_schedule(workers: int) -> Schedule:
+    """The reference run_backward order (runtime.cpp:605-651) as an explicit
+    schedule: the ring task table plus a GradKV message per direct pair."""
+    return _build(workers, 2)
+
+
+def build_balanced_backward_schedule(workers: int) -> Schedule:
+    """Load-balanced backward (extension): the balanced task
+    table; direct pairs exchange KV/GradKV, helpers receive the owner's
+    (q, dO, lse, D) bundle as the Q message and return dq as the Partial."""
+    return _build(workers, 3)
+
+
+def validate_backward(s: Schedule) -> list:
+    """validate() plus GradKV coverage of every direct pair."""
+    return validate(s, backward=True)
+
+
+def validate(s: Schedule, backward: bool = False) -> list:
     """schedule.cpp:121-258: the list of violation messages (empty = valid)."""
     tasks, msgs = s.flat()
     ta = (C.c_int32 * max(len(tasks), 1))(*tasks)
     ma = (C.c_int32 * max(len(msgs), 1))(*msgs)
     lib = _lib.lib()
-    n = lib.da_schedule_validate(s.workers, len(s.steps), ta, len(tasks) // 6, ma, len(msgs) // 4)
+    fn = lib.da_schedule_validate_backward if backward else lib.da_schedule_validate
+    n = fn(s.workers, len(s.steps), ta, len(tasks) // 6, ma, len(msgs) // 4)
     if n < 0:
         raise ConfigError(lib.da_last_error().decode())
     if n == 0:

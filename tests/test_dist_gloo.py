@@ -64,18 +64,19 @@ class OracleBackend:
         return torch.stack(outs), torch.stack(lses)
 
     def bwd_aux(self, d_out, out):
-        return None  # the oracle's block_attn_backward recomputes D (flashcore.hpp:294)
+        return torch.stack([torch.from_numpy(O.backward_aux(d_out[i].numpy(), out[i].numpy()))
+                            for i in range(out.shape[0])])
 
-    def grads(self, q, k, v, out, lse, d_out, d_vec, mask, dq, dk, dv, accumulate_kv):
+    def grads(self, q, k, v, lse, d_out, d_vec, mask, dq, dk, dv, accumulate_kv):
         h, hk = q.shape[0], k.shape[0]
         if not accumulate_kv:
             dk.zero_()
             dv.zero_()
         for i in range(h):
             j = i * hk // h
-            gq, gk, gv = O.block_attn_backward(q[i].numpy(), k[j].numpy(), v[j].numpy(),
-                                               out[i].numpy(), lse[i].numpy(), d_out[i].numpy(),
-                                               mask, self.scale)
+            gq, gk, gv = O.block_attn_backward_with_d(q[i].numpy(), k[j].numpy(), v[j].numpy(),
+                                                      d_vec[i].numpy(), lse[i].numpy(),
+                                                      d_out[i].numpy(), mask, self.scale)
             dq[i] += torch.from_numpy(gq)
             dk[j] += torch.from_numpy(gk)
             dv[j] += torch.from_numpy(gv)
@@ -92,7 +93,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, n, d, heads, schedule, outdir):
+def _worker(rank, world, port, n, d, heads, schedule, bwd_schedule, outdir):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     tdist.init_process_group("gloo", rank=rank, world_size=world)
@@ -105,7 +106,7 @@ def _worker(rank, world, port, n, d, heads, schedule, outdir):
         rt = DistRuntime(rank, world, backend=OracleBackend(d), transport=Transport(),
                          device=torch.device("cpu"))
         out, lse = rt.forward(t(q), t(k), t(v), schedule)
-        dq, dk, dv = rt.backward(t(do))
+        dq, dk, dv = rt.backward(t(do), bwd_schedule)
         np.savez(os.path.join(outdir, f"r{rank}.npz"), out=out.numpy(), lse=lse.numpy(),
                  dq=dq.numpy(), dk=dk.numpy(), dv=dv.numpy(),
                  held=rt.trace["max_remote_chunks_held"])
@@ -113,18 +114,22 @@ def _worker(rank, world, port, n, d, heads, schedule, outdir):
         tdist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,schedule", [(2, "balanced"), (3, "balanced"), (4, "balanced"),
-                                            (4, "ring")])
-def test_dist_runtime_gloo_bit_exact(world, schedule):
+@pytest.mark.parametrize("world,schedule,bwd", [(2, "balanced", "ring"), (3, "balanced", "balanced"),
+                                                (4, "balanced", "balanced"), (4, "ring", "ring"),
+                                                (5, "balanced", "balanced")])
+def test_dist_runtime_gloo_bit_exact(world, schedule, bwd):
     n, d, heads = 16 * world, 8, 2
     with tempfile.TemporaryDirectory() as td:
-        mp.spawn(_worker, args=(world, _free_port(), n, d, heads, schedule, td), nprocs=world,
+        mp.spawn(_worker, args=(world, _free_port(), n, d, heads, schedule, bwd, td), nprocs=world,
                  join=True)
         res = [np.load(os.path.join(td, f"r{r}.npz")) for r in range(world)]
     q, k, v, do = O.make_inputs(0, world, n, d, heads, bf16=True)
     for h in range(heads):
         out, lse, _ = O.run_forward(q[h], k[h], v[h], world, schedule)
-        dq, dk, dv, _ = O.run_backward(q[h], k[h], v[h], out, lse, do[h], world)
+        if bwd == "ring":  # the reference's own order
+            dq, dk, dv, _ = O.run_backward(q[h], k[h], v[h], out, lse, do[h], world)
+        else:
+            dq, dk, dv, _ = O.run_backward_sched(q[h], k[h], v[h], out, lse, do[h], world, bwd)
         got = {f: np.concatenate([r[f][h] for r in res], 0) for f in ("out", "lse", "dq", "dk", "dv")}
         assert np.array_equal(got["out"], out)
         assert np.array_equal(got["lse"], lse)

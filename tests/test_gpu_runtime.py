@@ -41,7 +41,8 @@ def test_device_make_shards_is_the_reference_index_map(cuda):
     assert np.array_equal(_np(_cat(shards, "d_out")), do)
 
 
-def _check_against_oracle(shards, P, n, sched, heads, trace_f=None, trace_b=None, heads_kv=None):
+def _check_against_oracle(shards, P, n, sched, heads, trace_f=None, trace_b=None, heads_kv=None,
+                          bwd="ring"):
     heads_kv = heads_kv or heads
     group = heads // heads_kv
     q, k, v, do = (_np(_cat(shards, f)) for f in ("q", "k", "v", "d_out"))
@@ -52,7 +53,10 @@ def _check_against_oracle(shards, P, n, sched, heads, trace_f=None, trace_b=None
     for h in range(heads):
         hk = h // group
         o_r, l_r, cf = O.run_forward(q[h], k[hk], v[hk], P, sched)
-        dq_r, dk_r, dv_r, cb = O.run_backward(q[h], k[hk], v[hk], o_r, l_r, do[h], P)
+        if bwd == "ring":
+            dq_r, dk_r, dv_r, cb = O.run_backward(q[h], k[hk], v[hk], o_r, l_r, do[h], P)
+        else:
+            dq_r, dk_r, dv_r, cb = O.run_backward_sched(q[h], k[hk], v[hk], o_r, l_r, do[h], P, bwd)
         assert _rel(out[h], o_r) < TOL, ("out", h)
         assert np.abs(lse[h] - l_r).max() < LSE_TOL, ("lse", h)
         assert _rel(dq[h], dq_r) < TOL, ("dq", h)
@@ -90,6 +94,17 @@ def test_worker_counts_balanced(cuda, P, n, heads):
     tb = run_backward(shards)
     torch.cuda.synchronize()
     _check_against_oracle(shards, P, n, "balanced", heads, tf, tb)
+
+
+@pytest.mark.parametrize("P,n", [(4, 4096), (5, 1280), (8, 2048)])
+def test_balanced_backward(cuda, P, n):
+    """Load-balanced backward (extension): same gradients, balanced pairs."""
+    from paper_2310_03294_b200.runtime import make_parity_shards, run_backward, run_forward
+    shards = make_parity_shards(2, P, n, 1, 128)
+    tf = run_forward(shards, "balanced")
+    tb = run_backward(shards, "balanced")
+    torch.cuda.synchronize()
+    _check_against_oracle(shards, P, n, "balanced", 1, tf, tb, bwd="balanced")
 
 
 def test_gqa_4q_2kv(cuda):

@@ -124,3 +124,35 @@ def test_json_csv_shape():
     csv = S.schedule_to_csv(s).splitlines()
     assert csv[0] == "step,worker,task,query_owner,kv_owner,helper"
     assert "1,4,rescale_merge,,,1" in csv
+
+
+def test_backward_schedules():
+    """Ring backward = the reference run_backward order; balanced backward is
+    the extension: same tasks as the balanced forward plus
+    GradKV returns, validated with the reference invariants + GradKV coverage."""
+    for p in range(1, 33):
+        rb = S.build_ring_backward_schedule(p)
+        bb = S.build_balanced_backward_schedule(p)
+        assert S.validate_backward(rb) == [] and S.validate_backward(bb) == []
+        # task tables are the forward ones
+        assert rb.steps == S.build_ring_schedule(p).steps
+        assert bb.steps == S.build_balanced_schedule(p).steps
+        grads = [m for m in bb.messages if m.kind == S.PayloadKind.GradKV]
+        direct = [t for st in bb.steps for t in st
+                  if t.kind == S.TaskKind.RemoteAttn and t.worker == t.query_owner]
+        assert len(grads) == len(direct)
+    b8 = S.build_balanced_backward_schedule(8)
+    assert S.expected_speedup(b8) == Fraction(36, 5)
+    assert S.expected_speedup(S.build_ring_backward_schedule(8)) == Fraction(9, 2)
+    # message accounting at P=6 (reference ring backward: 15 GradKV, test_runtime.cpp:234-268)
+    r6 = S.build_ring_backward_schedule(6)
+    assert sum(1 for m in r6.messages if m.kind == S.PayloadKind.GradKV) == 15
+
+
+def test_backward_validator_flags_missing_grad():
+    s = S.build_balanced_backward_schedule(6)
+    idx = [i for i, m in enumerate(s.messages) if m.kind == S.PayloadKind.GradKV][0]
+    del s.messages[idx]
+    assert any("never returned" in m for m in S.validate_backward(s))
+    # and the forward validator rejects stray GradKV messages
+    assert any("grad_kv" in m for m in S.validate(S.build_ring_backward_schedule(3)))

@@ -24,10 +24,11 @@ for _ in range(3):
 torch.cuda.synchronize()
 t = tr.view(64, 16).cpu().tolist()
 names = ["mma:wait_p", "mma:p_ok", "mma:ds_ok", "mma:drained", "mma:do_ok",
-         "cmp:A0", "cmp:A1", "cmp:B0", "cmp:B1", "drn:dq_ok", "drn:arrive", "drn:end"]
+         "cmp:A0", "cmp:A1", "cmp:B0", "cmp:B1", "drn:dq_ok", "drn:arrive", "drn:end",
+         "B:ldtm", "B:math", "B:stores", "B:fence"]
 base = t[0][0]
 for it in range(4, 16):
     row = t[it]
     t0 = row[1]
     print(f"it {it:2d} period {t[it+1][1]-row[1]:6d}  " +
-          " ".join(f"{names[s]}={row[s]-t0:+6d}" for s in (2, 3, 4, 5, 6, 7, 8, 9, 10, 11)))
+          " ".join(f"{names[s]}={row[s]-t0:+6d}" for s in (2, 3, 4, 5, 6, 7, 12, 13, 14, 15, 8, 9, 10, 11)))

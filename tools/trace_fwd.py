@@ -1,0 +1,26 @@
+"""Prints the forward kernel's per-iteration clock64 timeline (CTA 0, DA_TRACE build)."""
+import ctypes as C
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2310_03294_b200 import _lib  # noqa: E402
+from paper_2310_03294_b200.flashcore import MaskMode, block_attn_update_final  # noqa: E402
+
+h, n = 32, int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+q, k, v = [(torch.rand(h, n, 128, device="cuda") * 2 - 1).to(torch.bfloat16) for _ in range(3)]
+tr = torch.zeros(64 * 16, dtype=torch.int64, device="cuda")
+_lib.lib().da_debug_set_fwd_trace(C.c_void_p(tr.data_ptr()))
+for _ in range(3):
+    block_attn_update_final(q, k, v, None, MaskMode.Diagonal)
+torch.cuda.synchronize()
+t = tr.view(64, 16).cpu().tolist()
+names = {0: "mma:loop", 7: "mma:v_ok", 8: "mma:k_ok", 1: "mma:p0_ok", 2: "mma:p1_ok",
+         3: "sm0:s_ok", 4: "sm0:p_done", 5: "sm1:s_ok", 6: "sm1:p_done"}
+for j in range(4, 20):
+    row = t[j]
+    t0 = row[0]
+    print(f"j {j:2d} period {t[j+1][0]-row[0]:6d}  " +
+          " ".join(f"{names[s]}={row[s]-t0:+6d}" for s in (7, 8, 3, 4, 1, 5, 6, 2)))
