@@ -110,8 +110,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   // ---- work: kv tiles with the most query tiles first (causal)
   const int n_q_tiles = (p.rows_q + kBM - 1) / kBM;
   const int n_kv_tiles = (p.rows_kv + kBN - 1) / kBN;
+#ifdef DA_HEAD_MINOR_GRID
   const int kv_head = blockIdx.x % p.h_kv;
-  const int jt = static_cast<int>(blockIdx.x / p.h_kv);  // ascending: diag-heavy first
+  const int jt = static_cast<int>(blockIdx.x / p.h_kv);
+#else
+  // head-major: the co-resident CTAs share one head's Q/dO/dQ in L2;
+  // within a head, kv tiles with the most query tiles launch first
+  const int kv_head = static_cast<int>(blockIdx.x / n_kv_tiles);
+  const int jt = static_cast<int>(blockIdx.x % n_kv_tiles);
+#endif
   const int group = p.h_q / p.h_kv;
   const int i0 = (p.mask == DA_MASK_DIAGONAL) ? jt : 0;
   const int n_i = n_q_tiles - i0;
