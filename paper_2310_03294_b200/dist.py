@@ -208,6 +208,137 @@ def backward_plan(schedule, worker: int) -> list[BwdStepPlan]:
     return plans
 
 
+# ----------------------------------------------------------------------------- trace
+_KIND = {0: "kv", 1: "q", 2: "partial", 3: "grad_kv"}
+
+
+class Recorder:
+    """Per-rank wall-clock trace in the reference's ExecutionTrace terms
+    (runtime.hpp:66-89): task events, messages (issue at the sender, arrival
+    at the receiver) and byte-exact counters. CUDA events on GPU (resolved
+    after the pass), perf_counter on CPU."""
+
+    def __init__(self, cuda: bool, group=None, enabled: bool = True):
+        import time
+        self.cuda = cuda
+        self.enabled = enabled
+        if enabled and tdist.is_initialized() and tdist.get_world_size(group) > 1:
+            tdist.barrier(group=group)  # common origin for every rank's clock
+        self.origin_wall = time.time()
+        self.t0 = self.mark()
+        self.events = []      # (label, m0, m1)
+        self.sends = []       # (key, mark)
+        self.arrivals = []    # (key, mark)
+        self.counters = {"kv_scalars": 0, "q_scalars": 0, "partial_scalars": 0, "grad_scalars": 0,
+                         "kv_messages": 0, "q_messages": 0, "partial_messages": 0,
+                         "grad_messages": 0, "kv_bytes": 0, "q_bytes": 0, "partial_bytes": 0,
+                         "grad_bytes": 0}
+        self.kernel_calls = 0
+
+    def mark(self):
+        if not self.enabled:
+            return None
+        if self.cuda:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            return e
+        import time
+        return time.time()
+
+    def _ms(self, m):
+        # CUDA: device time since this rank's barrier-aligned origin;
+        # CPU: host wall clock (shared by the ranks of one host)
+        if self.cuda:
+            return self.t0.elapsed_time(m)
+        return (m - self.t0) * 1e3
+
+    def task(self, label, m0, m1, attention=True):
+        self.kernel_calls += 1 if attention else 0
+        if self.enabled:
+            self.events.append((label, m0, m1))
+
+    def send(self, step, kind, frm, to, mark):
+        if self.enabled:
+            self.sends.append(((step, kind, frm, to), mark))
+
+    def arrive(self, step, kind, frm, to, mark, tensors, scalars_per_head_row=None):
+        """Counted at the consumer like count_message (runtime.cpp:50-83):
+        scalars are elements, bytes are the payload's storage."""
+        if self.enabled:
+            self.arrivals.append(((step, kind, frm, to), mark))
+        name = {0: "kv", 1: "q", 2: "partial", 3: "grad"}[kind]
+        self.counters[f"{name}_scalars"] += sum(t.numel() for t in tensors)
+        self.counters[f"{name}_bytes"] += sum(t.numel() * t.element_size() for t in tensors)
+        self.counters[f"{name}_messages"] += 1
+
+    def resolve(self):
+        if self.cuda and self.enabled:
+            torch.cuda.synchronize()
+        return {"events": [(lbl, self._ms(a), self._ms(b)) for lbl, a, b in self.events],
+                "sends": [(k, self._ms(m)) for k, m in self.sends],
+                "arrivals": [(k, self._ms(m)) for k, m in self.arrivals],
+                "counters": dict(self.counters), "kernel_calls": self.kernel_calls}
+
+
+def gather_trace(rec: "Recorder", rank: int, world: int, held: int, group=None):
+    """All ranks contribute; rank 0 returns the reference-schema trace dict
+    (trace_to_json, runtime.cpp:752-782) and everyone else None."""
+    mine = rec.resolve()
+    if not rec.enabled:
+        raise StateError("the pass ran without trace=True")
+    if not rec.cuda:  # re-base host wall clocks on the earliest origin
+        mine["origin"] = rec.origin_wall
+    mine["rank"] = rank
+    mine["held"] = held
+    allr = [None] * world
+    if world > 1:
+        tdist.all_gather_object(allr, mine, group=group)
+    else:
+        allr = [mine]
+    if rank != 0:
+        return None
+    if "origin" in allr[0]:
+        base = min(r["origin"] for r in allr)
+        for r in allr:
+            sh = (r["origin"] - base) * 1e3
+            r["events"] = [(lbl, a + sh, b + sh) for lbl, a, b in r["events"]]
+            r["sends"] = [(k, t + sh) for k, t in r["sends"]]
+            r["arrivals"] = [(k, t + sh) for k, t in r["arrivals"]]
+    issue = {k: t for r in allr for k, t in r["sends"]}
+    msgs = []
+    for r in allr:
+        for k, t in r["arrivals"]:
+            msgs.append({"t_issue": issue.get(k, t), "t_arrive": t, "kind": _KIND[k[1]],
+                         "from": k[2], "to": k[3]})
+    msgs.sort(key=lambda m: (m["t_issue"], m["from"], m["to"]))
+    counters = {}
+    for r in allr:
+        for c, v in r["counters"].items():
+            counters[c] = counters.get(c, 0) + v
+    workers = [{"worker": r["rank"] + 1,
+                "events": [{"t0": a, "t1": b, "task": lbl} for lbl, a, b in r["events"]]}
+               for r in sorted(allr, key=lambda r: r["rank"])]
+    makespan = max((e["t1"] for w in workers for e in w["events"]), default=0.0)
+    return {"workers": workers, "messages": msgs, "counters": counters,
+            "attention_kernel_calls": sum(r["kernel_calls"] for r in allr),
+            "max_remote_chunks_held": max(r["held"] for r in allr), "makespan": makespan,
+            "time_unit": "ms"}
+
+
+def trace_to_json(trace: dict) -> str:
+    import json
+    return json.dumps(trace, indent=2)
+
+
+def trace_to_csv(trace: dict) -> str:
+    """runtime.cpp:784-797 columns."""
+    lines = ["worker,t0,t1,task"]
+    for w in trace["workers"]:
+        for e in w["events"]:
+            lines.append(f"{w['worker']},{e['t0']!r},{e['t1']!r},{e['task']}")
+    return "\n".join(lines) + "\n"
+
+
 # ----------------------------------------------------------------------------- runtime
 class DistRuntime:
     """Sequence-parallel attention for ONE rank holding chunk `rank` of the sequence.
@@ -241,7 +372,8 @@ class DistRuntime:
         self.trace["messages_sent"] += 1
         self.trace["bytes_sent"] += sum(t.numel() * t.element_size() for t in tensors)
 
-    def forward(self, q, k, v, schedule: str = "balanced", overlap: bool = True):
+    def forward(self, q, k, v, schedule: str = "balanced", overlap: bool = True,
+                trace: bool = False):
         P, w = self.world, self.worker
         sched = build_balanced_schedule(P) if schedule == "balanced" else build_ring_schedule(P)
         viol = validate(sched)
@@ -251,6 +383,7 @@ class DistRuntime:
         h, rows, d = q.shape
         hk = k.shape[0]
         be, tr = self.backend, self.transport
+        rec = self.rec = Recorder(tr.nccl, tr.group, trace)
         acc, _ = be.new_acc(h, rows, d, self._buf("acc", (h * rows * (d + 2),), be.acc_dtype))
         have_acc = False
         # receive slots: double-buffered (prefetch depth 1)
@@ -265,12 +398,15 @@ class DistRuntime:
             """sends of my immutable KV/Q for step t + the receive my step-t action needs."""
             p = plans[t]
             sends, recvs = [], []
+            mk = rec.mark()
             for dst in p.kv_sends:
                 sends += [(k, dst - 1), (v, dst - 1)]
                 self._sent(k, v)
+                rec.send(t, 0, w, dst, mk)
             for dst in p.q_sends:
                 sends.append((q, dst - 1))
                 self._sent(q)
+                rec.send(t, 1, w, dst, mk)
             if p.action == "direct":
                 ks, vs = kv_slot[t % 2]
                 recvs += [(ks, p.peer - 1), (vs, p.peer - 1)]
@@ -289,18 +425,28 @@ class DistRuntime:
             handle.wait()
             cur_held = (1 if p.action in ("direct", "help") else 0) + (1 if nxt is not None and plans[t + 1].action in ("direct", "help") else 0)
             held = max(held, cur_held)
+            m0 = rec.mark()
+            if p.action == "direct":
+                rec.arrive(t, 0, p.peer, w, m0, kv_slot[t % 2])
+            elif p.action == "help":
+                rec.arrive(t, 1, p.peer, w, m0, [q_slot[t % 2]])
             if p.action == "local":
                 be.update(q, k, v, acc if have_acc else None, "diagonal", acc)
                 have_acc = True
+                rec.task("local_attn", m0, rec.mark())
             elif p.action == "direct":
                 ks, vs = kv_slot[t % 2]
                 be.update(q, ks, vs, acc if have_acc else None, "full", acc)
                 have_acc = True
+                rec.task(f"remote_attn q={w} kv={p.peer}", m0, rec.mark())
             elif p.action == "help":
                 if part_handle is not None:
                     part_handle.wait()  # the previous partial has left this buffer
                 be.update(q_slot[t % 2], k, v, None, "full", part)
+                m1 = rec.mark()
+                rec.task(f"helper_attn q={p.peer} kv={w}", m0, m1)
                 part_handle = tr.exchange([(part_pk, p.peer - 1)], [])
+                rec.send(t, 2, w, p.peer, m1)
                 self._sent(part_pk)
             # merges of partials computed by helpers this step
             for hw in p.merges:
@@ -309,8 +455,11 @@ class DistRuntime:
                     buf = self._buf(f"part_recv{hw}", (h * rows * (d + 2),), be.acc_dtype)
                     recv_part[hw] = buf
                 tr.exchange([], [(buf, hw - 1)]).wait()
+                m0 = rec.mark()
+                rec.arrive(t, 2, hw, w, m0, [buf])
                 pa, _ = be.new_acc(h, rows, d, buf)
                 be.merge(acc, pa)
+                rec.task(f"rescale_merge helper={hw}", m0, rec.mark(), attention=False)
             if not overlap and t + 1 < len(plans):
                 nxt = post_operands(t + 1)
             pending = nxt if nxt is not None else _Done()
@@ -321,7 +470,7 @@ class DistRuntime:
         self.saved = (q, k, v, out, lse)
         return out, lse
 
-    def backward(self, d_out, schedule: str = "ring", overlap: bool = True):
+    def backward(self, d_out, schedule: str = "ring", overlap: bool = True, trace: bool = False):
         """Backward reusing the saved O and LSE (no forward recompute).
 
         schedule="ring": the reference order (runtime.cpp:605-651);
@@ -340,6 +489,7 @@ class DistRuntime:
         if viol:
             raise ScheduleError(f"invalid schedule: {viol[0]} ({len(viol)} violations)")
         plans = backward_plan(sched, w)
+        rec = self.rec_bwd = Recorder(tr.nccl, tr.group, trace)
         gd = be.grad_dtype
         dq = self._buf("dq", (h, rows, d), gd)
         dk = self._buf("dk", (hk, rows, d), gd)
@@ -360,12 +510,15 @@ class DistRuntime:
         def post_operands(t):
             p = plans[t]
             sends, recvs = [], []
+            mk = rec.mark()
             for dst in p.kv_sends:
                 sends += [(k, dst - 1), (v, dst - 1)]
                 self._sent(k, v)
+                rec.send(t, 0, w, dst, mk)
             for dst in p.q_sends:
                 sends += [(q, dst - 1), (d_out, dst - 1), (lse, dst - 1), (d_vec, dst - 1)]
                 self._sent(q, d_out, lse, d_vec)
+                rec.send(t, 1, w, dst, mk)
             if p.action == "direct":
                 ks, vs = kv_slot[t % 2]
                 recvs += [(ks, p.peer - 1), (vs, p.peer - 1)]
@@ -382,21 +535,31 @@ class DistRuntime:
             held = max(held, (1 if p.action in ("direct", "help") else 0) +
                        (1 if nxt is not None and plans[t + 1].action in ("direct", "help") else 0))
             sends = []
+            m0 = rec.mark()
             if p.action == "local":
                 be.grads(q, k, v, lse, d_out, d_vec, "diagonal", dq, dk, dv, accumulate_kv=True)
+                rec.task("bwd_local", m0, rec.mark())
             elif p.action == "direct":
+                rec.arrive(t, 0, p.peer, w, m0, kv_slot[t % 2])
                 ks, vs = kv_slot[t % 2]
                 gk, gv = g_send[t % 2]
                 be.grads(q, ks, vs, lse, d_out, d_vec, "full", dq, gk, gv, accumulate_kv=False)
+                m1 = rec.mark()
+                rec.task(f"bwd_remote kv={p.peer}", m0, m1)
                 sends += [(gk, p.peer - 1), (gv, p.peer - 1)]
                 self._sent(gk, gv)
+                rec.send(t, 3, w, p.peer, m1)
             elif p.action == "help":
+                rec.arrive(t, 1, p.peer, w, m0, bundle[t % 2])
                 bq, bdo, blse, bD = bundle[t % 2]
                 gq = q_send[t % 2]
                 gq.zero_()
                 be.grads(bq, k, v, blse, bdo, bD, "full", gq, dk, dv, accumulate_kv=True)
+                m1 = rec.mark()
+                rec.task(f"bwd_helper q={p.peer}", m0, m1)
                 sends.append((gq, p.peer - 1))
                 self._sent(gq)
+                rec.send(t, 2, w, p.peer, m1)
             recvs = [(g_recv[0], s - 1) for s in p.gradkv_from[:1]] + \
                     [(g_recv[1], s - 1) for s in p.gradkv_from[:1]]
             part_bufs = []
@@ -409,16 +572,28 @@ class DistRuntime:
             # results leave right after their kernels; waiting also retires the
             # send buffers before they are rewritten two steps later
             tr.exchange(sends, recvs).wait()
+            m2 = rec.mark()
             if p.gradkv_from:
+                rec.arrive(t, 3, p.gradkv_from[0], w, m2, g_recv)
                 be.add_(dk, g_recv[0])
                 be.add_(dv, g_recv[1])
-            for buf in part_bufs:
+            for hw, buf in zip(p.merges, part_bufs):
+                rec.arrive(t, 2, hw, w, m2, [buf])
                 be.add_(dq, buf)
             if not overlap and t + 1 < len(plans):
                 nxt = post_operands(t + 1)
             pending = nxt if nxt is not None else _Done()
         self.trace["max_remote_chunks_held_bwd"] = held
         return dq, dk, dv
+
+    def forward_trace(self, group=None):
+        """Collective: rank 0 gets the forward pass trace (reference schema)."""
+        return gather_trace(self.rec, self.rank, self.world, self.trace["max_remote_chunks_held"],
+                            group)
+
+    def backward_trace(self, group=None):
+        return gather_trace(self.rec_bwd, self.rank, self.world,
+                            self.trace.get("max_remote_chunks_held_bwd", 0), group)
 
 
 # ----------------------------------------------------------------------------- bench (N > 1)

@@ -137,3 +137,71 @@ def test_dist_runtime_gloo_bit_exact(world, schedule, bwd):
         assert np.array_equal(got["dk"], dk)
         assert np.array_equal(got["dv"], dv)
     assert max(int(r["held"]) for r in res) <= 2  # residency bound with prefetch
+
+
+def _trace_worker(rank, world, port, n, d, heads, heads_kv, schedule, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2310_03294_b200.dist import DistRuntime, Transport, trace_to_json
+        q, k, v, do = O.make_inputs(1, world, n, d, heads, bf16=True)
+        rows = n // world
+        sl = slice(rank * rows, (rank + 1) * rows)
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a[:, sl]))  # noqa: E731
+        rt = DistRuntime(rank, world, backend=OracleBackend(d), transport=Transport(),
+                         device=torch.device("cpu"))
+        rt.forward(t(q), t(k[:heads_kv]), t(v[:heads_kv]), schedule, trace=True)
+        rt.backward(t(do), schedule, trace=True)
+        tf, tb = rt.forward_trace(), rt.backward_trace()
+        if rank == 0:
+            with open(os.path.join(outdir, "fwd.json"), "w") as fh:
+                fh.write(trace_to_json(tf))
+            with open(os.path.join(outdir, "bwd.json"), "w") as fh:
+                fh.write(trace_to_json(tb))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,schedule,heads,heads_kv", [(4, "ring", 2, 2), (6, "balanced", 4, 2)])
+def test_wall_clock_trace_schema_and_counters(world, schedule, heads, heads_kv):
+    """wall-clock trace in the reference schema (runtime.cpp:752-782)
+    with byte-exact counters; the measured forward KV volume equals the analyzer's
+    seq_parallel_forward_kv_volume_nd (analyzer.cpp:39-44) exactly."""
+    import json
+    from fractions import Fraction
+    from paper_2310_03294_b200 import schedule as S
+    n, d = 8 * world, 8
+    with tempfile.TemporaryDirectory() as td:
+        mp.spawn(_trace_worker, args=(world, _free_port(), n, d, heads, heads_kv, schedule, td),
+                 nprocs=world, join=True)
+        tf = json.loads(open(os.path.join(td, "fwd.json")).read())
+        tb = json.loads(open(os.path.join(td, "bwd.json")).read())
+    for tr in (tf, tb):
+        assert set(tr) >= {"workers", "messages", "counters", "attention_kernel_calls",
+                           "max_remote_chunks_held", "makespan"}
+        assert [w["worker"] for w in tr["workers"]] == list(range(1, world + 1))
+        for w in tr["workers"]:
+            for e in w["events"]:
+                assert 0.0 <= e["t0"] <= e["t1"] <= tr["makespan"] + 1e-6
+        for m in tr["messages"]:
+            assert m["t_issue"] <= m["t_arrive"] + 0.5  # host clocks of one machine
+        assert tr["attention_kernel_calls"] == world * (world + 1) // 2
+    sched = S.build_ring_schedule(world) if schedule == "ring" else S.build_balanced_schedule(world)
+    kinds = {0: "kv", 1: "q", 2: "partial", 3: "grad_kv"}
+    want = sorted((kinds[int(m.kind)], m.from_, m.to) for m in sched.messages)
+    assert sorted((m["kind"], m["from"], m["to"]) for m in tf["messages"]) == want
+    c = tf["counters"]
+    rows = n // world
+    # scalars per the reference's payload sizes (runtime.cpp:50-59) times heads
+    assert c["kv_scalars"] == c["kv_messages"] * 2 * rows * d * heads_kv
+    assert c["q_scalars"] == c["q_messages"] * rows * d * heads
+    assert c["partial_scalars"] == c["partial_messages"] * rows * (d + 2) * heads
+    assert c["kv_bytes"] == 8 * c["kv_scalars"]  # float64 payloads in this CPU test
+    if schedule == "ring":
+        vol = Fraction(c["kv_scalars"], world * n * d * heads)
+        assert vol == Fraction(world - 1, world) * Fraction(heads_kv, heads)
+    gradkv = sum(1 for m in tb["messages"] if m["kind"] == "grad_kv")
+    direct = sum(1 for st in sched.steps for t_ in st
+                 if t_.kind == S.TaskKind.RemoteAttn and t_.worker == t_.query_owner)
+    assert gradkv == direct == tb["counters"]["grad_messages"]
