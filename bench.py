@@ -177,12 +177,13 @@ def run_single(args):
                          torch.empty(heads, n, D, device=dev))
 
     ev = {k_: [] for k_ in ("fwd", "aux", "bwd")}
+    dflag = torch.zeros(1, dtype=torch.int32, device=dev)  # checked once after the timed loop
 
     def step(record=False):
         if record:
             e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
             e[0].record(stream)
-        out = F.block_attn_update_final(q, k, v, None, F.MaskMode.Diagonal)
+        out = F.block_attn_update_final(q, k, v, None, F.MaskMode.Diagonal, degenerate_flag=dflag)
         if record:
             e[1].record(stream)
         dvec = F.backward_aux(d_out, out.o)
@@ -209,29 +210,23 @@ def run_single(args):
         end.record(stream)
         torch.cuda.synchronize()
     ms = start.elapsed_time(end) / args.steps
+    F.check_degenerate(dflag)
     fl = flops_fwd_bwd(n, heads)
     tflops = fl / (ms * 1e-3) / 1e12
     t_fwd = statistics.mean(a.elapsed_time(b) for a, b in ev["fwd"])
     t_bwd = statistics.mean(a.elapsed_time(b) for a, b in ev["bwd"])
     t_aux = statistics.mean(a.elapsed_time(b) for a, b in ev["aux"])
 
-    # ---- e2e: host (pinned) inputs -> device -> fwd+bwd -> bf16 grads -> host
+    # ---- e2e: host (pinned) inputs -> device -> fwd+bwd -> bf16 grads -> host,
+    # through the public host-buffer API (copies overlapped per head group)
+    from paper_2310_03294_b200.pipeline import HostAttention
     hq, hk, hv, hdo = (t.cpu().pin_memory() for t in (q, k, v, d_out))
-    hdq = torch.empty(heads, n, D, dtype=torch.bfloat16).pin_memory()
-    hdk = torch.empty_like(hdq).pin_memory()
-    hdv = torch.empty_like(hdq).pin_memory()
-    dq16, dk16, dv16 = (torch.empty(heads, n, D, dtype=torch.bfloat16, device=dev) for _ in range(3))
+    hdq, hdk, hdv = (torch.empty(heads, n, D, dtype=torch.bfloat16).pin_memory() for _ in range(3))
+    del grads
+    ha = HostAttention(heads, n, D, heads_per_group=args.heads_per_group, device=dev)
 
     def e2e_step():
-        dq_, dk_, dv_ = q, k, v  # device staging reused
-        dq_.copy_(hq, non_blocking=True)
-        dk_.copy_(hk, non_blocking=True)
-        dv_.copy_(hv, non_blocking=True)
-        d_out.copy_(hdo, non_blocking=True)
-        step()
-        for src, dst16, host in ((grads.dq, dq16, hdq), (grads.dk, dk16, hdk), (grads.dv, dv16, hdv)):
-            dst16.copy_(src)
-            host.copy_(dst16, non_blocking=True)
+        ha(hq, hk, hv, hdo, hdq, hdk, hdv, sync=False)
 
     for _ in range(2):
         e2e_step()
@@ -243,9 +238,10 @@ def run_single(args):
         e2e_step()
     e2.record(stream)
     torch.cuda.synchronize()
+    F.check_degenerate(ha.flag)
     ms_e2e = s2.elapsed_time(e2) / e_steps
-    h2d = 4 * heads * n * D * 2
-    d2h = 3 * heads * n * D * 2
+    h2d = ha.bytes_in
+    d2h = ha.bytes_out
 
     peak, peak_sus, src = peaks()
     # dominant kernel: the backward chunk kernel
@@ -275,8 +271,9 @@ def run_single(args):
                      "algorithmic_flops_per_launch": dom_flops},
         "e2e": {"value": fl / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
-                "path": "flashcore.block_attn_update_final + backward_aux + block_attn_backward "
-                        "(C ABI) with pinned-host q/k/v/dO in and bf16 dQ/dK/dV out"},
+                "path": "pipeline.HostAttention (flashcore.block_attn_update_final + backward_aux + "
+                        "block_attn_backward over the C ABI): pinned-host q/k/v/dO in, bf16 "
+                        "dQ/dK/dV out, copies overlapped per group of %d heads" % args.heads_per_group},
         "gpu_launches": 3 * args.steps,
         "clocks": clk.summary(),
     }
@@ -306,6 +303,7 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seq", type=int, default=SEQ)
     ap.add_argument("--heads", type=int, default=H)
+    ap.add_argument("--heads-per-group", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)
     if args.warmup < 3:

@@ -99,8 +99,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const __grid_constant__ CUtensorMap tmap_do,
                     const __grid_constant__ CUtensorMap tmap_dq, const BwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment (SW128) by offsetting the __shared__ symbol itself, so
+  // the compiler keeps the shared address space (STS/LDS, not generic ST/LD)
+  uint8_t* smem = smem_raw + smem_align_pad(smem_raw);
   Bars* bars = reinterpret_cast<Bars*>(smem + SmemLayout::bars);
   float* vecs = reinterpret_cast<float*>(smem + SmemLayout::vecs);
 
@@ -167,8 +168,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   // 4 x 32 x 16 = 2048 (-> 144) and the two compute WGs 8 x 32 x 8 = 2048 (-> 136).
   if (warp >= 12) setmaxnreg_dec<96>();
 
-  auto it_head = [&](int it) { return kv_head * group + it / n_i; };
-  auto it_qtile = [&](int it) { return i0 + it % n_i; };
+  // iteration it -> (query head, query tile) = (kv_head*group + it / n_i,
+  // i0 + it % n_i), stepped incrementally (no integer division in the loops)
+  struct ItCursor {
+    int hq, qt, i0, q_end;
+    __device__ __forceinline__ void next() {
+      if (++qt == q_end) { qt = i0; ++hq; }
+    }
+  };
+  const ItCursor cur0{kv_head * group, i0, i0, n_q_tiles};
 
   if (warp == 13) {
     // ===================== loader =====================
@@ -180,11 +188,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_load_3d(smem + SmemLayout::v, &tmap_v, &bars->kv_full, 0, jt * kBN, kv_head);
       tma_load_3d(smem + SmemLayout::v + kHalfTile, &tmap_v, &bars->kv_full, 64, jt * kBN, kv_head);
     }
-    for (int it = 0; it < n_it; ++it) {
+    ItCursor cur = cur0;
+    for (int it = 0; it < n_it; ++it, cur.next()) {
       const int st = it & 1;
       const uint32_t ph = (it >> 1) & 1;
-      const int hq = it_head(it);
-      const int row0 = it_qtile(it) * kBM;
+      const int hq = cur.hq;
+      const int row0 = cur.qt * kBM;
       mbar_wait(&bars->q_empty[st], ph ^ 1);
       if (lane == 0) {
         mbar_arrive_expect_tx(&bars->q_full[st], kTileBytes);
@@ -315,9 +324,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     setmaxnreg_inc<144>();
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
     const int dcol = warp * 32 + lane;  // head-dim index = TMEM lane of dQ^T
-    for (int it = 0; it < n_it; ++it) {
-      const int hq = it_head(it);
-      const int row0 = it_qtile(it) * kBM;
+    ItCursor cur = cur0;
+    for (int it = 0; it < n_it; ++it, cur.next()) {
+      const int hq = cur.hq;
+      const int row0 = cur.qt * kBM;
       mbar_wait(&bars->dq_full, it & 1);
       BWD_TRACE(warp == 0 && lane == 0, it, 9);
       tc_fence_after();
@@ -382,9 +392,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float sl2 = p.scale_log2;
     uint8_t* ds_smem = smem + SmemLayout::ds + half * kHalfTile + r * 128;
 
-    for (int it = 0; it < n_it; ++it) {
+    ItCursor cur = cur0;
+    for (int it = 0; it < n_it; ++it, cur.next()) {
       const int st = it & 1;
-      const bool diag = (p.mask == DA_MASK_DIAGONAL) && (it_qtile(it) == jt);
+      const bool diag = (p.mask == DA_MASK_DIAGONAL) && (cur.qt == jt);
       const float* lse2 = vecs + st * 256 + half * 64;
       const float* dvec = vecs + st * 256 + 128 + half * 64;
       mbar_wait(&bars->vec_full[st], (it >> 1) & 1);  // lse/D rows visible

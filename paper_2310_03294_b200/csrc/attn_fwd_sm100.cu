@@ -84,8 +84,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const __grid_constant__ CUtensorMap tmap_k,
                     const __grid_constant__ CUtensorMap tmap_v, const FwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment (SW128) by offsetting the __shared__ symbol itself, so
+  // the compiler keeps the shared address space (STS/LDS, not generic ST/LD)
+  uint8_t* smem = smem_raw + smem_align_pad(smem_raw);
   Bars* bars = reinterpret_cast<Bars*>(smem + SmemLayout::bars);
 
   const uint32_t warp = warp_id();

@@ -22,6 +22,11 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// bytes to add to a dynamic-smem symbol to reach the next 1024-byte boundary
+__device__ __forceinline__ uint32_t smem_align_pad(const void* base) {
+  return (1024u - (smem_u32(base) & 1023u)) & 1023u;
+}
+
 __device__ __forceinline__ uint32_t warp_id() {
   return __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
 }

@@ -76,7 +76,7 @@ def _req(t: torch.Tensor, dtype, name: str):
                         f"on {t.device} (contiguous={t.is_contiguous()})")
 
 
-def _fwd(q, k, v, acc_in, mask, scale, finalize, acc_out=None, stream=None):
+def _fwd(q, k, v, acc_in, mask, scale, finalize, acc_out=None, stream=None, degenerate_flag=None):
     _req(q, torch.bfloat16, "q"); _req(k, torch.bfloat16, "k"); _req(v, torch.bfloat16, "v")
     h_q, rows_q, d = q.shape
     h_kv, rows_kv, _ = k.shape
@@ -89,8 +89,10 @@ def _fwd(q, k, v, acc_in, mask, scale, finalize, acc_out=None, stream=None):
     if finalize:
         out = AttnOutput(torch.empty(h_q, rows_q, d, dtype=torch.bfloat16, device=q.device),
                          torch.empty(h_q, rows_q, dtype=torch.float32, device=q.device))
-        flag = torch.zeros(1, dtype=torch.int32, device=q.device)
-        a.o_out, a.lse_out, a.degenerate_flag = _ptr(out.o), _ptr(out.lse), _ptr(flag)
+        # a caller-owned flag defers the DegenerateRowError check (no stream sync)
+        flag = torch.zeros(1, dtype=torch.int32, device=q.device) if degenerate_flag is None else None
+        dflag = flag if degenerate_flag is None else degenerate_flag
+        a.o_out, a.lse_out, a.degenerate_flag = _ptr(out.o), _ptr(out.lse), _ptr(dflag)
     else:
         out = acc_out if acc_out is not None else AttnAccumulator(
             torch.empty(h_q, rows_q, d, dtype=torch.float32, device=q.device),
@@ -119,9 +121,20 @@ def block_attn_update(q, k, v, acc: AttnAccumulator | None, mask: MaskMode,
 
 
 def block_attn_update_final(q, k, v, acc: AttnAccumulator | None, mask: MaskMode,
-                            scale: float | None = None, stream=None) -> AttnOutput:
-    """block_attn_update followed by finalize in the same kernel (the paper's `last` flag)."""
-    return _fwd(q, k, v, acc, mask, scale, True, None, stream)
+                            scale: float | None = None, stream=None, *,
+                            degenerate_flag: torch.Tensor | None = None) -> AttnOutput:
+    """block_attn_update followed by finalize in the same kernel (the paper's `last` flag).
+
+    Without `degenerate_flag` a degenerate row raises DegenerateRowError here
+    (one stream sync). With a caller-owned int32 device flag the check is
+    deferred to ``check_degenerate(flag)``, so pipelined callers never sync.
+    """
+    return _fwd(q, k, v, acc, mask, scale, True, None, stream, degenerate_flag)
+
+
+def check_degenerate(flag: torch.Tensor, stream=None) -> None:
+    """Raises DegenerateRowError (finalize, flashcore.hpp:233-235) if `flag` was set."""
+    check(_lib.lib().da_check_degenerate(_ptr(flag), _stream(stream)))
 
 
 def rescale(a: AttnAccumulator, b: AttnAccumulator, *, out: AttnAccumulator | None = None,

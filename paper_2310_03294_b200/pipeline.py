@@ -1,0 +1,114 @@
+"""Host-buffer attention step with PCIe transfers overlapped per head group.
+
+The reference's public path takes host matrices (Eigen, runtime.hpp:32-41)
+and returns host gradients; its runtime overlaps the next chunk's transfer
+with the current chunk's compute (prefetch depth 1, runtime.cpp:280-284,
+427-431). ``HostAttention`` applies the same idea to the host<->HBM copies
+of a full causal forward+backward on one GPU: the heads are split into
+groups, and while group g computes (forward with fused finalize, backward
+preprocess, backward, bf16 conversion), group g+1's q/k/v/dO are in flight
+host->device on one copy stream and group g-1's dQ/dK/dV device->host on
+another. Heads are independent, so the grouping changes no arithmetic: the
+result is the same bits as the ungrouped launch on the whole tensor.
+
+Degenerate rows are checked once per call through a shared device flag
+(``flashcore.check_degenerate``) instead of one stream sync per group.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from . import flashcore as F
+from .errors import ShapeError, check
+
+
+class HostAttention:
+    """One causal fwd+bwd over pinned host tensors [heads, rows, 128].
+
+    Device buffers are allocated once per shape and reused across calls.
+    ``heads_per_group`` trades pipeline fill/drain (smaller groups) against
+    wave quantisation of each launch (larger groups).
+    """
+
+    def __init__(self, heads: int, rows: int, d: int = 128, heads_per_group: int = 4,
+                 device="cuda"):
+        if heads % heads_per_group != 0:
+            raise ShapeError(f"heads ({heads}) must be a multiple of heads_per_group "
+                             f"({heads_per_group})")
+        self.heads, self.rows, self.d, self.hg = heads, rows, d, heads_per_group
+        dev = torch.device(device)
+        bf = dict(dtype=torch.bfloat16, device=dev)
+        f32 = dict(dtype=torch.float32, device=dev)
+        self.q, self.k, self.v, self.d_out = (torch.empty(heads, rows, d, **bf) for _ in range(4))
+        self.dq = torch.empty(heads, rows, d, **f32)
+        self.dk = torch.empty(heads, rows, d, **f32)
+        self.dv = torch.empty(heads, rows, d, **f32)
+        self.dq16, self.dk16, self.dv16 = (torch.empty(heads, rows, d, **bf) for _ in range(3))
+        self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.h2d = torch.cuda.Stream(dev)
+        self.d2h = torch.cuda.Stream(dev)
+        self.out = None
+        self.lse = None
+
+    @property
+    def bytes_in(self) -> int:
+        return 4 * self.heads * self.rows * self.d * 2
+
+    @property
+    def bytes_out(self) -> int:
+        return 3 * self.heads * self.rows * self.d * 2
+
+    def _convert(self, src: torch.Tensor, dst: torch.Tensor, stream) -> None:
+        check(_lib.lib().da_convert_f32_bf16(F._ptr(src), F._ptr(dst), src.numel(),
+                                             F._stream(stream)))
+
+    def __call__(self, hq, hk, hv, hdo, hdq, hdk, hdv, *, sync: bool = True):
+        """q/k/v/dO pinned host bf16 in; dQ/dK/dV pinned host bf16 out.
+
+        Returns after the last device->host copy completed when ``sync``;
+        raises DegenerateRowError if any query row attended to no key.
+        """
+        for t in (hq, hk, hv, hdo, hdq, hdk, hdv):
+            if t.shape != (self.heads, self.rows, self.d) or t.dtype != torch.bfloat16:
+                raise ShapeError("HostAttention: host tensors must be bf16 "
+                                 f"[{self.heads}, {self.rows}, {self.d}]")
+        comp = torch.cuda.current_stream()
+        self.flag.zero_()
+        n_groups = self.heads // self.hg
+        in_ready = [torch.cuda.Event() for _ in range(n_groups)]
+        out_ready = [torch.cuda.Event() for _ in range(n_groups)]
+        # the previous call's readers of the device buffers are on `comp`
+        self.h2d.wait_stream(comp)
+        with torch.cuda.stream(self.h2d):
+            for g in range(n_groups):
+                sl = slice(g * self.hg, (g + 1) * self.hg)
+                for dst, src in ((self.q, hq), (self.k, hk), (self.v, hv), (self.d_out, hdo)):
+                    dst[sl].copy_(src[sl], non_blocking=True)
+                in_ready[g].record(self.h2d)
+        outs, lses = [], []
+        for g in range(n_groups):
+            sl = slice(g * self.hg, (g + 1) * self.hg)
+            comp.wait_event(in_ready[g])
+            q, k, v, do = self.q[sl], self.k[sl], self.v[sl], self.d_out[sl]
+            out = F.block_attn_update_final(q, k, v, None, F.MaskMode.Diagonal, stream=comp,
+                                            degenerate_flag=self.flag)
+            dvec = F.backward_aux(do, out.o, stream=comp)
+            grads = F.ChunkGrads(self.dq[sl], self.dk[sl], self.dv[sl])
+            grads.dq.zero_()
+            F.block_attn_backward(q, k, v, out.o, out.lse, do, F.MaskMode.Diagonal, d_vec=dvec,
+                                  grads=grads, stream=comp)
+            for src, dst in ((self.dq, self.dq16), (self.dk, self.dk16), (self.dv, self.dv16)):
+                self._convert(src[sl], dst[sl], comp)
+            out_ready[g].record(comp)
+            self.d2h.wait_event(out_ready[g])
+            with torch.cuda.stream(self.d2h):
+                for src, dst in ((self.dq16, hdq), (self.dk16, hdk), (self.dv16, hdv)):
+                    dst[sl].copy_(src[sl], non_blocking=True)
+            outs.append(out.o)
+            lses.append(out.lse)
+        comp.wait_stream(self.d2h)
+        self.out, self.lse = outs, lses  # the rematerialisation state (saved O, LSE) per group
+        if sync:
+            F.check_degenerate(self.flag, stream=comp)
+        return hdq, hdk, hdv

@@ -132,3 +132,39 @@ def test_single_gpu_fwd_bwd_32k_sampled(cuda):
     torch.cuda.synchronize()
     assert torch.isfinite(grads.dq).all() and torch.isfinite(grads.dk).all()
     assert torch.isfinite(grads.dv).all()
+
+
+@pytest.mark.parametrize("h,n,hpg", [(4, 1024, 2), (6, 700, 3), (2, 256, 2)])
+def test_host_pipeline_matches_direct_calls(cuda, h, n, hpg):
+    """pipeline.HostAttention (pinned host in/out, per-head-group overlap) computes
+    the same step as the ungrouped device calls: dK/dV bit-exact (deterministic
+    in-CTA reductions), dQ within one bf16 ulp (fp32 reduction order differs)."""
+    from paper_2310_03294_b200 import flashcore as F
+    from paper_2310_03294_b200.pipeline import HostAttention
+    q, k, v = _qkv(h, n, seed=h * n)
+    do = _qkv(h, n, seed=h * n + 1)[0]
+    out = F.block_attn_update_final(q, k, v, None, F.MaskMode.Diagonal)
+    g = F.block_attn_backward(q, k, v, out.o, out.lse, do, F.MaskMode.Diagonal)
+    ref = [x.to(torch.bfloat16).cpu() for x in (g.dq, g.dk, g.dv)]
+    host_in = [x.cpu().pin_memory() for x in (q, k, v, do)]
+    host_out = [torch.empty(h, n, 128, dtype=torch.bfloat16).pin_memory() for _ in range(3)]
+    ha = HostAttention(h, n, heads_per_group=hpg)
+    for _ in range(2):  # second call reuses the device buffers
+        ha(*host_in, *host_out)
+    assert torch.equal(host_out[1], ref[1]) and torch.equal(host_out[2], ref[2])
+    assert rel_err(host_out[0].float(), ref[0].float()) < 1e-2
+    o_ref, _ = attention_ref(q, k, v, True)
+    assert rel_err(torch.cat(ha.out, 0), o_ref) < TOL
+
+
+def test_host_pipeline_degenerate_rows_raise(cuda):
+    """A finalize over a row that attended to no key raises DegenerateRowError
+    (flashcore.hpp:233-235) even with the deferred (sync-free) flag."""
+    from paper_2310_03294_b200 import flashcore as F
+    from paper_2310_03294_b200.errors import DegenerateRowError
+    q, k, v = _qkv(2, 128, nk=128)
+    flag = torch.zeros(1, dtype=torch.int32, device=cuda)
+    F.block_attn_update_final(q, k[:, :0].contiguous(), v[:, :0].contiguous(), None,
+                              F.MaskMode.Full, degenerate_flag=flag)
+    with pytest.raises(DegenerateRowError):
+        F.check_degenerate(flag)
