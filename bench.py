@@ -303,7 +303,7 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seq", type=int, default=SEQ)
     ap.add_argument("--heads", type=int, default=H)
-    ap.add_argument("--heads-per-group", type=int, default=4)
+    ap.add_argument("--heads-per-group", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)
     if args.warmup < 3:

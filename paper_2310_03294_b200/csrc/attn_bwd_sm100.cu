@@ -16,7 +16,8 @@
 //   S^T  = K Q^T          (SS, M=kv,  N=q)  -> S region
 //   dP^T = V dO^T         (SS, M=kv,  N=q)  -> dP region
 //   dV  += P^T dO         (TS, A = P^T in TMEM, B = dO MN-major)
-//   dK  += dS^T Q         (TS, A = dS^T in TMEM, B = Q MN-major)
+//   dK  += dS^T Q         (TS, A = dS^T in TMEM, B = Q MN-major; -DDA_BWD_DS_SMEM:
+//                          SS from the smem dS^T tile, dQ^T issued first)
 //   dQ^T = K^T dS^T       (SS, A = K MN-major, B = dS^T smem MN-major) -> dP region
 // Computing dQ transposed puts the head dim on TMEM lanes, so a drain warp
 // reduces 32 consecutive floats of one dQ row per instruction (128 B): per-row
@@ -44,6 +45,13 @@ namespace bwd {
 #else
 #define BWD_TRACE(cond, it, slot) \
   do {                            \
+  } while (0)
+#endif
+#ifdef DA_TRACE
+#define BWD_PROBE(k) mma_commit(&bars->tb[k])
+#else
+#define BWD_PROBE(k) \
+  do {               \
   } while (0)
 #endif
 
@@ -88,6 +96,9 @@ struct Bars {
   uint64_t dq_full;
   uint64_t dq_drained;
   uint64_t acc_full;
+#ifdef DA_TRACE
+  uint64_t tb[5];  // MMA completion probes: dV, S(next), dK, dQ, dP(next)
+#endif
   uint32_t tmem_base;
 };
 static_assert(sizeof(Bars) <= 256, "barrier block");
@@ -143,6 +154,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bars->dq_full, 1);
       mbar_init(&bars->dq_drained, 128);
       mbar_init(&bars->acc_full, 1);
+#ifdef DA_TRACE
+      for (int k = 0; k < 5; ++k) mbar_init(&bars->tb[k], 1);
+#endif
       fence_barrier_init();
     }
   } else if (warp == 13) {
@@ -224,8 +238,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       float* lse2 = vecs + st * 256;
       float* dvec = lse2 + 128;
-      *reinterpret_cast<float4*>(lse2 + lane * 4) = make_float4(l2[0], l2[1], l2[2], l2[3]);
-      *reinterpret_cast<float4*>(dvec + lane * 4) = make_float4(dd[0], dd[1], dd[2], dd[3]);
+      // stored negated: the compute warps add them with packed FFMA2/FADD2
+      *reinterpret_cast<float4*>(lse2 + lane * 4) = make_float4(-l2[0], -l2[1], -l2[2], -l2[3]);
+      *reinterpret_cast<float4*>(dvec + lane * 4) = make_float4(-dd[0], -dd[1], -dd[2], -dd[3]);
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->vec_full[st]);
     }
@@ -280,6 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         gemm_ts(tmem + 0, tmem + kColS, do_addr, it > 0);
         mma_commit(&bars->do_empty);
+        BWD_PROBE(0);
         // next S^T (overwrites P only after dV has consumed it: in-order pipe)
         if (has_next) {
           const int st1 = (it + 1) & 1;
@@ -287,21 +303,42 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           gemm_kk(tmem + kColS, k_addr, q_addr + st1 * kTileBytes);
           mma_commit(&bars->s_full);
+          BWD_PROBE(1);
         }
-        // dK += dS^T Q
         mbar_wait(&bars->ds_full, it & 1);
         BWD_TRACE(true, it, 2);
         tc_fence_after();
+        auto issue_dq = [&]() {
+          // dQ^T = K^T dS^T  (A = K MN-major, B = dS^T MN-major): head dim on lanes
+#pragma unroll
+          for (int kk = 0; kk < kBN / 16; ++kk) {
+            mma_ss(tmem + kColDP, make_sdesc_sw128(k_addr + kk * 2048, kHalfTile, 1024),
+                   make_sdesc_sw128(ds_addr + kk * 2048, kHalfTile, 1024), idesc_mnmn,
+                   kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&bars->dq_full);
+          BWD_PROBE(3);
+        };
+#ifndef DA_BWD_DS_SMEM
+        // dK += dS^T Q (A = dS^T in TMEM, so dQ^T may only overwrite it after)
         gemm_ts(tmem + 128, tmem + kColDP, q_addr + st * kTileBytes, it > 0);
         mma_commit(&bars->q_empty[st]);
-        // dQ^T = K^T dS^T  (A = K MN-major, B = dS^T MN-major): head dim on lanes
+        BWD_PROBE(2);
+        issue_dq();
+#else
+        // dQ^T first: its drain (and the next dP^T behind it) then overlaps dK.
+        // dP^T(it) has left TMEM (phase B loaded it before signalling ds_full)
+        issue_dq();
+        // dK += dS^T Q: A = dS^T from smem (K-major: kv rows, q contiguous), B = Q MN-major
 #pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk) {
-          mma_ss(tmem + kColDP, make_sdesc_sw128(k_addr + kk * 2048, kHalfTile, 1024),
-                 make_sdesc_sw128(ds_addr + kk * 2048, kHalfTile, 1024), idesc_mnmn,
-                 kk > 0 ? 1u : 0u);
+        for (int kk = 0; kk < kBM / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * kHalfTile + (kk & 3) * 32;
+          mma_ss(tmem + 128, make_sdesc_sw128(ds_addr + off, 16, 1024),
+                 make_sdesc_sw128(q_addr + st * kTileBytes + kk * 2048, kHalfTile, 1024), idesc_kmn,
+                 (it > 0 || kk > 0) ? 1u : 0u);
         }
-        mma_commit(&bars->dq_full);
+        mma_commit(&bars->q_empty[st]);
+#endif
         // next dP^T once dQ^T has left TMEM
         if (has_next) {
           mbar_wait(&bars->dq_drained, it & 1);
@@ -311,19 +348,34 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           gemm_kk(tmem + kColDP, v_addr, do_addr);
           mma_commit(&bars->dp_full);
+          BWD_PROBE(4);
         }
       }
       mma_commit(&bars->acc_full);
     }
   } else if (warp >= 14) {
     // idle warps of the MMA/loader warpgroup
+#ifdef DA_TRACE
+    if (warp == 14 && lane == 0 && p.trace != nullptr && blockIdx.x == 0) {
+      for (int it = 0; it < n_it && it < 64; ++it) {
+        const bool nx = it + 1 < n_it;
+        for (int k = 0; k < 5; ++k) {
+          if ((k == 1 || k == 4) && !nx) continue;
+          mbar_wait(&bars->tb[k], it & 1);
+          p.trace[1024 + it * 8 + k] = clock64();
+        }
+      }
+    }
+#endif
   } else if (warp < 4) {
     // ===================== dQ drain =====================
     // all 128 columns are pulled out of TMEM before the region is released,
     // so the next dP^T MMA waits only for the loads, not for the reductions
     setmaxnreg_inc<144>();
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+#ifndef DA_BWD_DQ_TMA
     const int dcol = warp * 32 + lane;  // head-dim index = TMEM lane of dQ^T
+#endif
     ItCursor cur = cur0;
     for (int it = 0; it < n_it; ++it, cur.next()) {
       const int hq = cur.hq;
@@ -408,25 +460,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld_32x32b_x32(s_tmem, sr[0]);
       tmem_ld_32x32b_x32(s_tmem + 32, sr[1]);
       tmem_ld_wait();
+      if (diag) {
+        // query column (half*64 + c) is visible from kv row r iff q >= r:
+        // masked scores become -inf (exactly zero probability) before the
+        // exponential, so the exp loop itself stays branch-free
+#pragma unroll
+        for (int c = 0; c < 64; ++c)
+          if (half * 64 + c < r) sr[c >> 5][c & 31] = __float_as_uint(-INFINITY);
+      }
       // P is carried to phase B as the same bf16 values the dV MMA consumes
       uint32_t pk[32];
 #pragma unroll
       for (int c = 0; c < 64; c += 4) {
-        const float4 l4 = *reinterpret_cast<const float4*>(lse2 + c);
-        float p0 = ex2_approx(fmaf(__uint_as_float(sr[c >> 5][(c + 0) & 31]), sl2, -l4.x));
-        float p1 = ex2_approx(fmaf(__uint_as_float(sr[c >> 5][(c + 1) & 31]), sl2, -l4.y));
-        float p2 = ex2_approx(fmaf(__uint_as_float(sr[c >> 5][(c + 2) & 31]), sl2, -l4.z));
-        float p3 = ex2_approx(fmaf(__uint_as_float(sr[c >> 5][(c + 3) & 31]), sl2, -l4.w));
-        if (diag) {
-          // query column (half*64 + c) is visible from kv row r iff q >= r
-          const int qc = half * 64 + c;
-          p0 = qc + 0 < r ? 0.f : p0;
-          p1 = qc + 1 < r ? 0.f : p1;
-          p2 = qc + 2 < r ? 0.f : p2;
-          p3 = qc + 3 < r ? 0.f : p3;
-        }
-        pk[c / 2] = pack_bf16x2(p0, p1);
-        pk[c / 2 + 1] = pack_bf16x2(p2, p3);
+        const float4 l4 = *reinterpret_cast<const float4*>(lse2 + c);  // -lse2
+        const float2 x01 = ffma2(make_float2(__uint_as_float(sr[c >> 5][(c + 0) & 31]),
+                                             __uint_as_float(sr[c >> 5][(c + 1) & 31])),
+                                 make_float2(sl2, sl2), make_float2(l4.x, l4.y));
+        const float2 x23 = ffma2(make_float2(__uint_as_float(sr[c >> 5][(c + 2) & 31]),
+                                             __uint_as_float(sr[c >> 5][(c + 3) & 31])),
+                                 make_float2(sl2, sl2), make_float2(l4.z, l4.w));
+        pk[c / 2] = pack_bf16x2(ex2_approx(x01.x), ex2_approx(x01.y));
+        pk[c / 2 + 1] = pack_bf16x2(ex2_approx(x23.x), ex2_approx(x23.y));
       }
       tmem_st_32x32b_x32(s_tmem, pk);
       tmem_st_wait();
@@ -446,18 +500,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t dsk[32];
 #pragma unroll
       for (int c = 0; c < 64; c += 4) {
-        const float4 d4 = *reinterpret_cast<const float4*>(dvec + c);
+        const float4 d4 = *reinterpret_cast<const float4*>(dvec + c);  // -D
         const uint32_t a = pk[c / 2], b = pk[c / 2 + 1];
-        const float s0 = __uint_as_float(a << 16) * (__uint_as_float(dr[c >> 5][(c + 0) & 31]) - d4.x);
-        const float s1 = __uint_as_float(a & 0xFFFF0000u) * (__uint_as_float(dr[c >> 5][(c + 1) & 31]) - d4.y);
-        const float s2 = __uint_as_float(b << 16) * (__uint_as_float(dr[c >> 5][(c + 2) & 31]) - d4.z);
-        const float s3 = __uint_as_float(b & 0xFFFF0000u) * (__uint_as_float(dr[c >> 5][(c + 3) & 31]) - d4.w);
-        dsk[c / 2] = pack_bf16x2(s0, s1);
-        dsk[c / 2 + 1] = pack_bf16x2(s2, s3);
+        const float2 t01 = fadd2(make_float2(__uint_as_float(dr[c >> 5][(c + 0) & 31]),
+                                             __uint_as_float(dr[c >> 5][(c + 1) & 31])),
+                                 make_float2(d4.x, d4.y));
+        const float2 t23 = fadd2(make_float2(__uint_as_float(dr[c >> 5][(c + 2) & 31]),
+                                             __uint_as_float(dr[c >> 5][(c + 3) & 31])),
+                                 make_float2(d4.z, d4.w));
+        const float2 s01 =
+            fmul2(make_float2(__uint_as_float(a << 16), __uint_as_float(a & 0xFFFF0000u)), t01);
+        const float2 s23 =
+            fmul2(make_float2(__uint_as_float(b << 16), __uint_as_float(b & 0xFFFF0000u)), t23);
+        dsk[c / 2] = pack_bf16x2(s01.x, s01.y);
+        dsk[c / 2 + 1] = pack_bf16x2(s23.x, s23.y);
       }
       BWD_TRACE(cw == 0 && lane == 0, it, 13);
-      // dS^T (bf16) -> TMEM (A operand of dK) and -> smem (B operand of dQ^T)
+      // dS^T (bf16) -> smem: A operand (K-major) of dK, B operand (MN-major) of dQ^T
+#ifndef DA_BWD_DS_SMEM
       tmem_st_32x32b_x32(dp_tmem, dsk);
+#endif
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch) {
         const int phys = ch ^ (r & 7);
@@ -466,7 +528,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       BWD_TRACE(cw == 0 && lane == 0, it, 14);
       fence_proxy_async_smem();
+#ifndef DA_BWD_DS_SMEM
       tmem_st_wait();
+#endif
       BWD_TRACE(cw == 0 && lane == 0, it, 15);
       tc_fence_before();
       mbar_arrive(&bars->ds_full);

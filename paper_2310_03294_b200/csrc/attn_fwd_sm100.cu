@@ -18,6 +18,8 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <type_traits>
+
 #include "kernels.h"
 #include "sm100_ptx.cuh"
 
@@ -49,6 +51,11 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #endif
 // every kEx2EmuMod-th pair of columns is exponentiated on the FMA pipe (0: none)
 constexpr int kEx2EmuMod = DA_FWD_EX2_EMU_MOD;
+#ifndef DA_FWD_NO_PINGPONG
+constexpr bool kMufuPingPong = true;
+#else
+constexpr bool kMufuPingPong = false;
+#endif
 
 struct SmemLayout {
   // all tiles 1024B aligned (SW128)
@@ -221,9 +228,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t ph1 = ((j + 1) / kStages) & 1;
         FWD_TRACE(true, j, 0);
         mbar_wait(&bars->v_full[s], ph);
-        FWD_TRACE(true, j, 7);
+
         if (has_next) mbar_wait(&bars->k_full[s1], ph1);
-        FWD_TRACE(true, j, 8);
+
         tc_fence_after();
         for (int t = 0; t < 2; ++t) {
           if (j < n_t[t]) {
@@ -261,12 +268,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     for (int j = 0; j < n_tiles; ++j) {
       mbar_wait(&bars->s_full[t], j & 1);
-      FWD_TRACE(quarter == 0 && lane == 0, j, 3 + 2 * t);
+      FWD_TRACE(quarter == 0 && lane == 0, j, 3 + 6 * t);
       tc_fence_after();
       uint32_t sr[4][32];
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(s_tmem + c * 32, sr[c]);
       tmem_ld_wait();
+      FWD_TRACE(quarter == 0 && lane == 0, j, 4 + 6 * t);
 
       if (p.debug_s != nullptr && j == 0 && t == 0 && blockIdx.x == 0) {
         // raw (unscaled, unmasked) scores of the first tile, for layout tests
@@ -280,24 +288,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       // masking: causal inside the diagonal tile, ragged kv tail
       const bool diag = (p.mask == DA_MASK_DIAGONAL) && (j == qt);
       const int kv_valid = p.rows_kv - j * kBN;  // columns >= kv_valid are padding
-      float mx = neg_inf;
-      if (diag || kv_valid < kBN) {
+      const bool masked_tile = diag || kv_valid < kBN;
+      if (masked_tile) {
         const int lim = diag ? min(row_in_tile + 1, kv_valid) : kv_valid;
 #pragma unroll
         for (int c = 0; c < 4; ++c)
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
+          for (int i = 0; i < 32; ++i)
             if (c * 32 + i >= lim) sr[c][i] = __float_as_uint(neg_inf);
-            mx = fmaxf(mx, __uint_as_float(sr[c][i]));
-          }
-      } else {
+      }
+      // row max as a tree of 8 independent chains (latency, not a 128-long chain)
+      float mx;
+      {
+        float mc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) mc[u] = __uint_as_float(sr[u >> 1][(u & 1) * 16]);
 #pragma unroll
         for (int c = 0; c < 4; ++c)
 #pragma unroll
-          for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(sr[c][i]));
+          for (int i = 0; i < 32; ++i) {
+            const int u = c * 2 + i / 16;
+            if ((i & 15) != 0) mc[u] = fmaxf(mc[u], __uint_as_float(sr[c][i]));
+          }
+        mx = fmaxf(fmaxf(fmaxf(mc[0], mc[1]), fmaxf(mc[2], mc[3])),
+                   fmaxf(fmaxf(mc[4], mc[5]), fmaxf(mc[6], mc[7])));
       }
       mx *= sl2;
-      const bool masked_tile = diag || kv_valid < kBN;
+      FWD_TRACE(quarter == 0 && lane == 0, j, 5 + 6 * t);
 
       float alpha = 1.f;
       const float m_new = fmaxf(m_run, mx);
@@ -308,34 +325,59 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const float neg_m = (m_run == neg_inf) ? 0.f : -m_run;
 
-      float rs = 0.f;
+      // P = 2^(s*scale*log2e - m): packed FFMA2 for the argument, packed FADD2
+      // row sums (4 independent accumulators); on unmasked tiles every
+      // kEx2EmuMod-th column pair is exponentiated on the FMA pipe
+      // 8 independent packed accumulators: no FADD2 dependency stalls
+      float2 rs2[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) rs2[u] = make_float2(0.f, 0.f);
       uint32_t pk[2][32];
-      if (masked_tile || kEx2EmuMod == 0) {
-        // exact zeros for masked entries: MUFU only
+      const float2 sl2x2 = make_float2(sl2, sl2);
+      const float2 nm2 = make_float2(neg_m, neg_m);
+      auto exp_tile = [&](auto emulate) {
+        constexpr bool kEmu = decltype(emulate)::value;
 #pragma unroll
         for (int c = 0; c < 4; ++c)
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
-            const float p0 = ex2_approx(fmaf(__uint_as_float(sr[c][i]), sl2, neg_m));
-            const float p1 = ex2_approx(fmaf(__uint_as_float(sr[c][i + 1]), sl2, neg_m));
-            rs += p0 + p1;
-            pk[c >> 1][(c & 1) * 16 + i / 2] = pack_bf16x2(p0, p1);
+            const float2 x = ffma2(
+                make_float2(__uint_as_float(sr[c][i]), __uint_as_float(sr[c][i + 1])), sl2x2, nm2);
+            const int pair = c * 16 + i / 2;
+            float2 pv;
+            if (kEmu && (pair % kEx2EmuMod) == kEx2EmuMod - 1) {
+              pv = ex2_emu2(x);
+            } else {
+              pv = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+            }
+            rs2[pair & 7] = fadd2(rs2[pair & 7], pv);
+            pk[c >> 1][(c & 1) * 16 + i / 2] = pack_bf16x2(pv.x, pv.y);
           }
-      } else {
-        // steady state: every kEx2EmuMod-th column pair on the FMA pipe
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            const float x0 = fmaf(__uint_as_float(sr[c][i]), sl2, neg_m);
-            const float x1 = fmaf(__uint_as_float(sr[c][i + 1]), sl2, neg_m);
-            const bool emu = kEx2EmuMod > 0 && ((c * 16 + i / 2) % kEx2EmuMod) == kEx2EmuMod - 1;
-            const float p0 = emu ? ex2_emu(x0) : ex2_approx(x0);
-            const float p1 = emu ? ex2_emu(x1) : ex2_approx(x1);
-            rs += p0 + p1;
-            pk[c >> 1][(c & 1) * 16 + i / 2] = pack_bf16x2(p0, p1);
-          }
+      };
+      // MUFU ping-pong: the two tiles' exponential loops take turns (named
+      // barriers 1/2, 256 threads = both softmax warpgroups), so each runs at
+      // the full ex2 rate while the tensor core works on the other tile.
+      // Turn order per j: tile 0, then tile 1 (counts match for n0 <= n1).
+      if (kMufuPingPong) {
+        if (t == 0 ? (j > 0 && j <= n1) : (j < n0)) named_bar_sync(1 + t, 256);
       }
+      FWD_TRACE(quarter == 0 && lane == 0, j, 6 + 6 * t);
+      // masked entries must give exact zeros: the MUFU path only
+      if (kEx2EmuMod == 0 || masked_tile) {
+        exp_tile(std::false_type{});
+      } else {
+        exp_tile(std::integral_constant<bool, (kEx2EmuMod > 0)>{});
+      }
+      if (kMufuPingPong) {
+        if (t == 0 ? (j < n1) : (j + 1 < n0)) named_bar_arrive(2 - t, 256);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) rs2[u] = fadd2(rs2[u], rs2[u + 4]);
+      rs2[0] = fadd2(rs2[0], rs2[2]);
+      rs2[1] = fadd2(rs2[1], rs2[3]);
+      rs2[0] = fadd2(rs2[0], rs2[1]);
+      const float rs = rs2[0].x + rs2[0].y;
+      FWD_TRACE(quarter == 0 && lane == 0, j, 7 + 6 * t);
       l_run = l_run * alpha + rs;
 
       // lazy O correction: only warps with a row whose max jumped
@@ -352,12 +394,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st_32x32b_x32(o_tmem + c * 32, orr);
         }
       }
+
       tmem_st_32x32b_x32(p_tmem, pk[0]);
       tmem_st_32x32b_x32(p_tmem + 32, pk[1]);
       tmem_st_wait();
+
       tc_fence_before();
       mbar_arrive(&bars->p_full[t]);
-      FWD_TRACE(quarter == 0 && lane == 0, j, 4 + 2 * t);
+      FWD_TRACE(quarter == 0 && lane == 0, j, 8 + 6 * t);
     }
 
     // ===================== epilogue =====================

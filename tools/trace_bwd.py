@@ -17,12 +17,13 @@ out = block_attn_update_final(q, k, v, None, MaskMode.Diagonal)
 dvec = backward_aux(do, out.o)
 g = ChunkGrads(torch.zeros(h, n, 128, device="cuda"), torch.empty(h, n, 128, device="cuda"),
                torch.empty(h, n, 128, device="cuda"))
-tr = torch.zeros(64 * 16, dtype=torch.int64, device="cuda")
+tr = torch.zeros(64 * 32, dtype=torch.int64, device="cuda")
 _lib.lib().da_debug_set_bwd_trace(C.c_void_p(tr.data_ptr()))
 for _ in range(3):
     block_attn_backward(q, k, v, out.o, out.lse, do, MaskMode.Diagonal, d_vec=dvec, grads=g)
 torch.cuda.synchronize()
-t = tr.view(64, 16).cpu().tolist()
+t = tr[:1024].view(64, 16).cpu().tolist()
+pr = tr[1024:].view(64, 16).cpu().tolist()
 names = ["mma:wait_p", "mma:p_ok", "mma:ds_ok", "mma:drained", "mma:do_ok",
          "cmp:A0", "cmp:A1", "cmp:B0", "cmp:B1", "drn:dq_ok", "drn:arrive", "drn:end",
          "B:ldtm", "B:math", "B:stores", "B:fence"]
@@ -32,3 +33,5 @@ for it in range(4, 16):
     t0 = row[1]
     print(f"it {it:2d} period {t[it+1][1]-row[1]:6d}  " +
           " ".join(f"{names[s]}={row[s]-t0:+6d}" for s in (2, 3, 4, 5, 6, 7, 12, 13, 14, 15, 8, 9, 10, 11)))
+    print("        done: " + " ".join(f"{nm}={pr[it][k]-t0:+6d}" for k, nm in
+                                      enumerate(("dV", "S+1", "dK", "dQ", "dP+1"))))

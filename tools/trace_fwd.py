@@ -17,10 +17,12 @@ for _ in range(3):
     block_attn_update_final(q, k, v, None, MaskMode.Diagonal)
 torch.cuda.synchronize()
 t = tr.view(64, 16).cpu().tolist()
-names = {0: "mma:loop", 7: "mma:v_ok", 8: "mma:k_ok", 1: "mma:p0_ok", 2: "mma:p1_ok",
-         3: "sm0:s_ok", 4: "sm0:p_done", 5: "sm1:s_ok", 6: "sm1:p_done"}
+names = {0: "mma:loop", 1: "mma:p0_ok", 2: "mma:p1_ok"}
+for tt in range(2):
+    for k, nm in enumerate(("s_ok", "ld", "max", "bar", "exp", "p_done")):
+        names[3 + 6 * tt + k] = f"sm{tt}:{nm}"
 for j in range(4, 20):
     row = t[j]
     t0 = row[0]
     print(f"j {j:2d} period {t[j+1][0]-row[0]:6d}  " +
-          " ".join(f"{names[s]}={row[s]-t0:+6d}" for s in (7, 8, 3, 4, 1, 5, 6, 2)))
+          " ".join(f"{names[s]}={row[s]-t0:+6d}" for s in (3, 4, 5, 6, 7, 8, 1, 9, 10, 11, 12, 13, 14, 2)))
