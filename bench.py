@@ -304,6 +304,8 @@ def main(argv=None):
     ap.add_argument("--seq", type=int, default=SEQ)
     ap.add_argument("--heads", type=int, default=H)
     ap.add_argument("--heads-per-group", type=int, default=2)
+    ap.add_argument("--fwd-schedule", default="balanced", choices=["ring", "balanced", "balanced_split"])
+    ap.add_argument("--bwd-schedule", default="balanced", choices=["ring", "balanced"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)
     if args.warmup < 3:

@@ -151,7 +151,8 @@ da_status da_convert_f32_bf16(const float* src, void* dst, int64_t n, void* stre
  *     kind: 0 LocalAttn, 1 RemoteAttn, 2 RescaleMerge, 3 Idle (TaskKind order)
  *     tasks appear step by step, P primaries ascending by worker then merges;
  *   messages[i] = {step, from, to, kind} (int32 x 4)
- *     kind: 0 KV, 1 Q, 2 PartialResult, 3 GradKV (PayloadKind order).
+ *     kind: 0 KV, 1 Q, 2 PartialResult, 3 GradKV (PayloadKind order),
+ *           4 KVHalf (half of a kv chunk's rows; DA_SCHEDULE_BALANCED_SPLIT).
  * Call once with NULL buffers to size them (counts are always written).
  * ------------------------------------------------------------------------ */
 typedef enum da_schedule_kind {
@@ -163,7 +164,15 @@ typedef enum da_schedule_kind {
    * §8(f)1): the forward task table with KV/GradKV for direct pairs,
    * Q = (q, dO, lse, D) bundle to the helper and Partial = dq contribution back. */
   DA_SCHEDULE_RING_BWD = 2,
-  DA_SCHEDULE_BALANCED_BWD = 3
+  DA_SCHEDULE_BALANCED_BWD = 3,
+  /* Forward extension (not in the reference): balanced with
+   * the even-P last step split. At t = P/2 helper p computes the pair
+   * (p + P/2, p) on the low half of its kv rows and the owner on the high
+   * half, so no worker idles; the step costs half a chunk pair. For
+   * RemoteAttn tasks the `helper` slot carries the kv row part:
+   * 0 whole chunk, 1 rows [0, c/2), 2 rows [c/2, c). The owner's half arrives
+   * as message kind 4 (KVHalf). Odd P: identical to DA_SCHEDULE_BALANCED. */
+  DA_SCHEDULE_BALANCED_SPLIT = 4
 } da_schedule_kind;
 
 da_status da_schedule_build(int workers, int kind, int32_t* steps_out, int32_t* tasks,

@@ -113,7 +113,11 @@ int dao_schedule_build(int P, int kind, int32_t* steps, int32_t* tasks, int64_t*
           push6(tasks, &nt, t, 3, p, 0, 0, 0);
         }
       }
-  } else { /* balanced, schedule.cpp:79-108 */
+  } else { /* balanced, schedule.cpp:79-108; kind 4 = the even-P split extension
+             * (SURVEY §8(f)2): at t = P/2 helper p takes pair (p + P/2, p) on the
+             * low half of its kv rows (part 1, in the helper slot of the task),
+             * the owner the high half (part 2) via a KVHalf (kind 4) message */
+    const int split = (kind == 4) && (P % 2 == 0);
     const int half = P / 2;
     *steps = half + 1;
     for (int p = 1; p <= P; ++p) push6(tasks, &nt, 0, 0, p, p, p, 0);
@@ -121,14 +125,15 @@ int dao_schedule_build(int P, int kind, int32_t* steps, int32_t* tasks, int64_t*
     for (int t = 1; t <= half; ++t) {
       int64_t nmg = 0;
       for (int p = 1; p <= P; ++p) {
+        const int last_split = split && t == half;
         if (p > t) {
-          push6(tasks, &nt, t, 1, p, p, p - t, 0);
-          push4(msgs, &nm, t, p - t, p, 0);
-        } else if (P % 2 == 0 && t == half) {
+          push6(tasks, &nt, t, 1, p, p, p - t, last_split ? 2 : 0);
+          push4(msgs, &nm, t, p - t, p, last_split ? 4 : 0);
+        } else if (P % 2 == 0 && t == half && !split) {
           push6(tasks, &nt, t, 3, p, 0, 0, 0);
         } else {
           const int owner = p + P - t;
-          push6(tasks, &nt, t, 1, p, owner, p, 0);
+          push6(tasks, &nt, t, 1, p, owner, p, last_split ? 1 : 0);
           push4(msgs, &nm, t, owner, p, 1);
           push4(msgs, &nm, t, p, owner, 2);
           push6(merges, &nmg, t, 2, owner, 0, 0, p);
@@ -381,6 +386,7 @@ static void count_msg(int64_t* c, int kind, int64_t rows, int64_t d) {
     case 1: c[1] += rows * d; ++c[5]; break;
     case 2: c[2] += rows * (d + 2); ++c[6]; break;
     case 3: c[3] += 2 * rows * d; ++c[7]; break;
+    case 4: c[0] += 2 * rows * d; ++c[4]; break; /* KVHalf: rows = the half */
   }
 }
 
@@ -419,12 +425,20 @@ int dao_run_forward(int P, int kind, int64_t n, int64_t d, const double* q, cons
                               d, ow, m + (w - 1) * rows, l + (w - 1) * rows, 0, scale, 16, 16);
       } else if (tk[2] == tk[3]) {
         const int r = tk[4];
+        /* kv row window: whole chunk, or the low/high half of the split step */
+        const int64_t lo = rows / 2;
+        const int64_t r0 = tk[5] == 2 ? lo : 0;
+        const int64_t nr = tk[5] == 0 ? rows : (tk[5] == 1 ? lo : rows - lo);
         held_any = 1;
-        count_msg(c, 0, rows, d);
-        dao_block_attn_update(q + (w - 1) * osz, rows, k + (r - 1) * osz, v + (r - 1) * osz, rows,
-                              d, ow, m + (w - 1) * rows, l + (w - 1) * rows, 1, scale, 16, 16);
+        count_msg(c, tk[5] == 0 ? 0 : 4, nr, d);
+        dao_block_attn_update(q + (w - 1) * osz, rows, k + (r - 1) * osz + r0 * d,
+                              v + (r - 1) * osz + r0 * d, nr, d, ow, m + (w - 1) * rows,
+                              l + (w - 1) * rows, 1, scale, 16, 16);
       } else {
         const int owner = tk[3];
+        const int64_t lo = rows / 2;
+        const int64_t r0 = tk[5] == 2 ? lo : 0;
+        const int64_t nr = tk[5] == 0 ? rows : (tk[5] == 1 ? lo : rows - lo);
         held_any = 1;
         count_msg(c, 1, rows, d);
         double* pw = po + (size_t)(w - 1) * osz;
@@ -433,9 +447,9 @@ int dao_run_forward(int P, int kind, int64_t n, int64_t d, const double* q, cons
           pm[(w - 1) * rows + r] = NEG_INF;
           pl[(w - 1) * rows + r] = 0.0;
         }
-        dao_block_attn_update(q + (owner - 1) * osz, rows, k + (w - 1) * osz, v + (w - 1) * osz,
-                              rows, d, pw, pm + (w - 1) * rows, pl + (w - 1) * rows, 1, scale, 16,
-                              16);
+        dao_block_attn_update(q + (owner - 1) * osz, rows, k + (w - 1) * osz + r0 * d,
+                              v + (w - 1) * osz + r0 * d, nr, d, pw, pm + (w - 1) * rows,
+                              pl + (w - 1) * rows, 1, scale, 16, 16);
       }
     }
     for (int64_t i = 0; i < nt; ++i) {

@@ -116,8 +116,11 @@ def make_inputs(seed: int, workers: int, n: int, d: int, heads: int, bf16: bool 
     return q, k, v, do
 
 
+_KINDS = {"ring": 0, "balanced": 1, "balanced_split": 4}
+
+
 def schedule_flat(workers: int, kind: str):
-    kind_i = 0 if kind == "ring" else 1
+    kind_i = _KINDS[kind]
     steps, nt, nm = C.c_int32(0), C.c_int64(0), C.c_int64(0)
     _ok(lib().dao_schedule_build(workers, kind_i, C.byref(steps), None, C.byref(nt), None,
                                  C.byref(nm)), "schedule")
@@ -211,7 +214,7 @@ def run_forward(q, k, v, workers: int, schedule: str):
     n, d = q.shape
     out, lse = np.empty((n, d)), np.empty(n)
     c = (C.c_int64 * 10)()
-    _ok(lib().dao_run_forward(workers, 0 if schedule == "ring" else 1, n, d, q, k, v, out, lse, c),
+    _ok(lib().dao_run_forward(workers, _KINDS[schedule], n, d, q, k, v, out, lse, c),
         "run_forward")
     return out, lse, list(c)
 

@@ -29,6 +29,8 @@ struct Workspace {
   std::vector<float*> o, m, l;  // per worker running accumulator
   std::vector<float*> po, pm, pl;  // per worker helper-partial slot
   std::vector<float*> dvec;       // per worker D (backward)
+  void* kv_half = nullptr;        // packed k, v row half (split schedule), bf16
+  size_t kv_half_bytes = 0;
   int* flag = nullptr;
   std::vector<void*> allocs;
 
@@ -37,6 +39,8 @@ struct Workspace {
     allocs.clear();
     o.clear(); m.clear(); l.clear(); po.clear(); pm.clear(); pl.clear(); dvec.clear();
     flag = nullptr;
+    kv_half = nullptr;
+    kv_half_bytes = 0;
     P = 0;
   }
   ~Workspace() { release(); }
@@ -77,6 +81,16 @@ struct Workspace {
 
 thread_local Workspace g_ws;
 
+// Packs rows [r0, r0 + n) of every head of a bf16 [h, rows, d] chunk into a
+// contiguous [h, n, d] buffer (a strided 2-D copy: one row block per head).
+cudaError_t pack_rows(const void* src, void* dst, int64_t h, int64_t rows, int64_t r0, int64_t n,
+                      int64_t d, cudaStream_t st) {
+  const size_t pitch_src = static_cast<size_t>(rows) * d * 2;
+  const size_t width = static_cast<size_t>(n) * d * 2;
+  return cudaMemcpy2DAsync(dst, width, static_cast<const char*>(src) + r0 * d * 2, pitch_src, width,
+                           h, cudaMemcpyDeviceToDevice, st);
+}
+
 da_status check_shards(const da_shards* s, bool backward) {
   if (s == nullptr) return set_error(DA_ERR_CONFIG, "null shards");
   if (s->workers < 1) return set_error(DA_ERR_CONFIG, "need at least 1 worker");
@@ -113,6 +127,7 @@ void count(da_counters& c, int kind, int64_t rows, int64_t d, int64_t heads) {
     case kMsgQ: c.q_scalars += rows * d * heads; ++c.q_messages; break;
     case kMsgPartial: c.partial_scalars += rows * (d + 2) * heads; ++c.partial_messages; break;
     case kMsgGradKV: c.grad_scalars += 2 * rows * d * heads; ++c.grad_messages; break;
+    case kMsgKVHalf: c.kv_scalars += 2 * rows * d * heads; ++c.kv_messages; break;
   }
 }
 
@@ -153,9 +168,12 @@ da_status da_run_forward(const da_shards* s, int schedule_kind, da_counters* cou
   da_status rc = check_shards(s, false);
   if (rc != DA_OK) return rc;
   const int P = s->workers;
-  if (schedule_kind != DA_SCHEDULE_RING && schedule_kind != DA_SCHEDULE_BALANCED)
+  if (schedule_kind != DA_SCHEDULE_RING && schedule_kind != DA_SCHEDULE_BALANCED &&
+      schedule_kind != DA_SCHEDULE_BALANCED_SPLIT)
     return set_error(DA_ERR_CONFIG, "unknown schedule kind");
-  const FlatSchedule sch = schedule_kind == DA_SCHEDULE_RING ? make_ring(P) : make_balanced(P);
+  const FlatSchedule sch = schedule_kind == DA_SCHEDULE_RING      ? make_ring(P)
+                           : schedule_kind == DA_SCHEDULE_BALANCED ? make_balanced(P)
+                                                                   : make_balanced_split(P);
   const auto errs = validate_flat(sch);
   if (!errs.empty())
     return set_error(DA_ERR_SCHEDULE, "invalid schedule: " + errs.front() + " (" +
@@ -178,6 +196,49 @@ da_status da_run_forward(const da_shards* s, int schedule_kind, da_counters* cou
       if (k.kind == kLocal) {
         rc = fwd_update(s, w, w, started[w - 1] ? o : nullptr, m, l, o, m, l, DA_MASK_DIAGONAL, st);
         started[w - 1] = true;
+      } else if (k.helper != kPartWhole) {  // split step: one half of the kv rows
+        const int64_t lo = s->rows / 2;
+        const int64_t r0 = k.helper == kPartLow ? 0 : lo;
+        const int64_t n = k.helper == kPartLow ? lo : s->rows - lo;
+        const size_t bytes = static_cast<size_t>(s->h_kv) * (s->rows - lo) * s->d * 2 * 2;
+        if (g_ws.kv_half_bytes < bytes) {
+          if (g_ws.kv_half) {
+            cudaFree(g_ws.kv_half);
+            for (auto& a : g_ws.allocs)
+              if (a == g_ws.kv_half) a = nullptr;
+          }
+          e = cudaMalloc(&g_ws.kv_half, bytes);
+          if (e != cudaSuccess) return cuda_error(e, "run_forward split workspace");
+          g_ws.allocs.push_back(g_ws.kv_half);
+          g_ws.kv_half_bytes = bytes;
+        }
+        void* kh = g_ws.kv_half;
+        void* vh = static_cast<char*>(g_ws.kv_half) + bytes / 2;
+        e = pack_rows(s->k[k.kv_owner - 1], kh, s->h_kv, s->rows, r0, n, s->d, st);
+        if (e == cudaSuccess) e = pack_rows(s->v[k.kv_owner - 1], vh, s->h_kv, s->rows, r0, n, s->d, st);
+        if (e != cudaSuccess) return cuda_error(e, "run_forward split pack");
+        da_fwd_args a{};
+        a.q = s->q[k.query_owner - 1];
+        a.k = kh;
+        a.v = vh;
+        a.h_q = s->h_q;
+        a.h_kv = s->h_kv;
+        a.rows_q = s->rows;
+        a.rows_kv = n;
+        a.d = s->d;
+        a.mask = DA_MASK_FULL;
+        me.acquire();
+        if (k.worker == k.query_owner) {  // owner: high half, accumulator in place
+          count(me.c, kMsgKVHalf, n, s->d, s->h_kv);
+          if (started[w - 1]) { a.o_in = o; a.m_in = m; a.l_in = l; }
+          a.o_acc = o; a.m_acc = m; a.l_acc = l;
+          started[w - 1] = true;
+        } else {  // helper: low half of its own kv, fresh partial
+          count(me.c, kMsgQ, s->rows, s->d, s->h_q);
+          a.o_acc = g_ws.po[w - 1]; a.m_acc = g_ws.pm[w - 1]; a.l_acc = g_ws.pl[w - 1];
+        }
+        rc = da_attn_fwd_chunk(&a, st);
+        me.release();
       } else if (k.worker == k.query_owner) {  // Direct: kv chunk of kv_owner
         me.acquire();
         count(me.c, kMsgKV, s->rows, s->d, s->h_kv);

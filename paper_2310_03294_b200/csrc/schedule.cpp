@@ -65,12 +65,45 @@ FlatSchedule make_balanced(int P) {
   return s;
 }
 
+FlatSchedule make_balanced_split(int P) {
+  if (P % 2 == 1) return make_balanced(P);
+  FlatSchedule s;
+  s.workers = P;
+  const int half = P / 2;
+  s.steps = half + 1;
+  for (int p = 1; p <= P; ++p) s.tasks.push_back({0, kLocal, p, p, p, 0});
+  for (int t = 1; t <= half; ++t) {
+    std::vector<Task> merges;
+    for (int p = 1; p <= P; ++p) {
+      if (p > t) {
+        if (t == half) {
+          // direct pair (p, p - P/2) on the high half of kv chunk p - P/2
+          s.tasks.push_back({t, kRemote, p, p, p - t, kPartHigh});
+          s.messages.push_back({t, p - t, p, kMsgKVHalf});
+        } else {
+          s.tasks.push_back({t, kRemote, p, p, p - t, kPartWhole});
+          s.messages.push_back({t, p - t, p, kMsgKV});
+        }
+      } else {
+        const int owner = p + P - t;
+        s.tasks.push_back({t, kRemote, p, owner, p, t == half ? kPartLow : kPartWhole});
+        s.messages.push_back({t, owner, p, kMsgQ});
+        s.messages.push_back({t, p, owner, kMsgPartial});
+        merges.push_back({t, kMerge, owner, 0, 0, p});
+      }
+    }
+    s.tasks.insert(s.tasks.end(), merges.begin(), merges.end());
+  }
+  return s;
+}
+
 static const char* kind_name(int k) {
   switch (k) {
     case kMsgKV: return "kv";
     case kMsgQ: return "q";
     case kMsgPartial: return "partial";
     case kMsgGradKV: return "grad_kv";
+    case kMsgKVHalf: return "kv_half";
   }
   return "?";
 }
@@ -82,7 +115,13 @@ std::vector<std::string> validate_flat(const FlatSchedule& s) {
     return errs;
   }
   const int P = s.workers;
-  std::map<std::pair<int, int>, int> pairs;  // (q, kv) -> times computed
+  // (q, kv) -> times each half of the kv rows was covered (low, high)
+  std::map<std::pair<int, int>, std::pair<int, int>> pairs;
+  auto cover = [&](int q, int kv, int part) {
+    auto& c = pairs[{q, kv}];
+    if (part != kPartHigh) ++c.first;
+    if (part != kPartLow) ++c.second;
+  };
   struct Pending {
     int step, owner, helper;
     bool merged;
@@ -111,7 +150,7 @@ std::vector<std::string> validate_flat(const FlatSchedule& s) {
       }
       if (k.kind == kLocal) {
         ++slots[k.worker];
-        ++pairs[{k.worker, k.worker}];
+        cover(k.worker, k.worker, kPartWhole);
       } else if (k.kind == kIdle) {
         ++slots[k.worker];
       } else if (k.kind == kRemote) {
@@ -120,9 +159,13 @@ std::vector<std::string> validate_flat(const FlatSchedule& s) {
           errs.push_back(st + std::to_string(t) + ": remote task with non-causal pair (q=" +
                          std::to_string(k.query_owner) + ", kv=" + std::to_string(k.kv_owner) +
                          ")");
-        ++pairs[{k.query_owner, k.kv_owner}];
+        const int part = k.helper;
+        if (part != kPartWhole && part != kPartLow && part != kPartHigh)
+          errs.push_back(st + std::to_string(t) + ": remote task with unknown kv part " +
+                         std::to_string(part));
+        cover(k.query_owner, k.kv_owner, part);
         if (k.worker == k.query_owner) {
-          if (!take(t, k.kv_owner, k.worker, kMsgKV))
+          if (!take(t, k.kv_owner, k.worker, part == kPartWhole ? kMsgKV : kMsgKVHalf))
             errs.push_back(st + std::to_string(t) + ": worker " + std::to_string(k.worker) +
                            " computes on kv chunk " + std::to_string(k.kv_owner) +
                            " that was never sent");
@@ -164,10 +207,15 @@ std::vector<std::string> validate_flat(const FlatSchedule& s) {
   for (int p = 1; p <= P; ++p)
     for (int r = 1; r <= p; ++r) {
       auto it = pairs.find({p, r});
-      const int n = it == pairs.end() ? 0 : it->second;
+      const int lo = it == pairs.end() ? 0 : it->second.first;
+      const int hi = it == pairs.end() ? 0 : it->second.second;
+      const int n = std::max(lo, hi);
       if (n == 0)
         errs.push_back("pair (q=" + std::to_string(p) + ", kv=" + std::to_string(r) +
                        ") is never computed");
+      else if (std::min(lo, hi) == 0)
+        errs.push_back("pair (q=" + std::to_string(p) + ", kv=" + std::to_string(r) +
+                       ") is only partly computed (" + (lo ? "low" : "high") + " half)");
       else if (n > 1)
         errs.push_back("pair (q=" + std::to_string(p) + ", kv=" + std::to_string(r) +
                        ") computed " + std::to_string(n) + " times");
@@ -243,6 +291,7 @@ da_status da_schedule_build(int workers, int kind, int32_t* steps_out, int32_t* 
     case DA_SCHEDULE_BALANCED: s = da::make_balanced(workers); break;
     case DA_SCHEDULE_RING_BWD: s = da::make_ring_backward(workers); break;
     case DA_SCHEDULE_BALANCED_BWD: s = da::make_balanced_backward(workers); break;
+    case DA_SCHEDULE_BALANCED_SPLIT: s = da::make_balanced_split(workers); break;
     default: return da::set_error(DA_ERR_CONFIG, "unknown schedule kind");
   }
   if (steps_out) *steps_out = s.steps;

@@ -10,8 +10,13 @@ namespace da {
 
 // TaskKind order of schedule.hpp:21
 enum : int32_t { kLocal = 0, kRemote = 1, kMerge = 2, kIdle = 3 };
-// PayloadKind order of schedule.hpp:45
-enum : int32_t { kMsgKV = 0, kMsgQ = 1, kMsgPartial = 2, kMsgGradKV = 3 };
+// PayloadKind order of schedule.hpp:45; KVHalf is the split-schedule extension
+enum : int32_t { kMsgKV = 0, kMsgQ = 1, kMsgPartial = 2, kMsgGradKV = 3, kMsgKVHalf = 4 };
+
+// Row part of a RemoteAttn task's kv chunk (carried in Task::helper, which the
+// reference only uses for RescaleMerge): the whole chunk, or the low / high
+// half of its rows (low = rows [0, c/2), high = [c/2, c)).
+enum : int32_t { kPartWhole = 0, kPartLow = 1, kPartHigh = 2 };
 
 struct Task {
   int32_t step, kind, worker, query_owner, kv_owner, helper;
@@ -30,6 +35,13 @@ struct FlatSchedule {
 
 FlatSchedule make_ring(int P);
 FlatSchedule make_balanced(int P);
+// Balanced schedule with the even-P last step split (extension):
+// at t = P/2 the reference leaves helpers 1..P/2 idle because owner p + P/2's
+// direct pair (p + P/2, p) is the helper's own pair. Here helper p computes that
+// pair on the LOW half of its kv rows (Q in, Partial out, merged by the owner)
+// and the owner computes it on the HIGH half (KVHalf message). Identical to
+// make_balanced for odd P.
+FlatSchedule make_balanced_split(int P);
 std::vector<std::string> validate_flat(const FlatSchedule& s);
 
 // Backward schedules (extension: the reference's backward is ring-only,

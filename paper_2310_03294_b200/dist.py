@@ -35,7 +35,8 @@ from dataclasses import dataclass
 import torch
 import torch.distributed as tdist
 
-from .schedule import (TaskKind, build_balanced_backward_schedule, build_balanced_schedule,
+from .schedule import (KVPart, TaskKind, build_balanced_backward_schedule,
+                       build_balanced_schedule, build_balanced_split_schedule,
                        build_ring_backward_schedule, build_ring_schedule, validate,
                        validate_backward)
 from .errors import ConfigError, ScheduleError, StateError
@@ -142,6 +143,8 @@ class StepPlan:
     kv_sends: tuple = ()     # destinations (1-based) of my KV this step
     q_sends: tuple = ()      # destinations of my Q this step
     merges: tuple = ()       # helpers (1-based) whose partial I merge this step, in order
+    part: int = 0            # kv rows of the pair: KVPart (split schedule extension)
+    kvh_sends: tuple = ()    # destinations of the high half of my KV rows (KVHalf)
 
 
 def forward_plan(schedule, worker: int) -> list[StepPlan]:
@@ -159,10 +162,13 @@ def forward_plan(schedule, worker: int) -> list[StepPlan]:
                     p.action, p.peer = "direct", task.kv_owner
                 else:
                     p.action, p.peer = "help", task.query_owner
+                p.part = int(task.kv_part)
             elif task.kind == TaskKind.RescaleMerge:
                 p.merges += (task.helper,)
         p.kv_sends = tuple(m.to for m in schedule.messages
                            if m.step == t and m.from_ == worker and int(m.kind) == 0)
+        p.kvh_sends = tuple(m.to for m in schedule.messages
+                            if m.step == t and m.from_ == worker and int(m.kind) == 4)
         p.q_sends = tuple(m.to for m in schedule.messages
                           if m.step == t and m.from_ == worker and int(m.kind) == 1)
         plans.append(p)
@@ -209,7 +215,7 @@ def backward_plan(schedule, worker: int) -> list[BwdStepPlan]:
 
 
 # ----------------------------------------------------------------------------- trace
-_KIND = {0: "kv", 1: "q", 2: "partial", 3: "grad_kv"}
+_KIND = {0: "kv", 1: "q", 2: "partial", 3: "grad_kv", 4: "kv_half"}
 
 
 class Recorder:
@@ -266,7 +272,7 @@ class Recorder:
         scalars are elements, bytes are the payload's storage."""
         if self.enabled:
             self.arrivals.append(((step, kind, frm, to), mark))
-        name = {0: "kv", 1: "q", 2: "partial", 3: "grad"}[kind]
+        name = {0: "kv", 1: "q", 2: "partial", 3: "grad", 4: "kv"}[kind]
         self.counters[f"{name}_scalars"] += sum(t.numel() for t in tensors)
         self.counters[f"{name}_bytes"] += sum(t.numel() * t.element_size() for t in tensors)
         self.counters[f"{name}_messages"] += 1
@@ -375,7 +381,11 @@ class DistRuntime:
     def forward(self, q, k, v, schedule: str = "balanced", overlap: bool = True,
                 trace: bool = False):
         P, w = self.world, self.worker
-        sched = build_balanced_schedule(P) if schedule == "balanced" else build_ring_schedule(P)
+        builders = {"balanced": build_balanced_schedule, "ring": build_ring_schedule,
+                    "balanced_split": build_balanced_split_schedule}
+        if schedule not in builders:
+            raise ConfigError(f"unknown forward schedule {schedule!r}")
+        sched = builders[schedule](P)
         viol = validate(sched)
         if viol:
             raise ScheduleError(f"invalid schedule: {viol[0]} ({len(viol)} violations)")
@@ -393,6 +403,20 @@ class DistRuntime:
         part_pk = self._buf("part_send", (h * rows * (d + 2),), be.acc_dtype)
         part, _ = be.new_acc(h, rows, d, part_pk)
         recv_part = {}
+        # split step (balanced_split): kv rows [0, lo) stay with the helper,
+        # [lo, rows) travel to the owner as one packed KVHalf message
+        lo = rows // 2
+        if any(p.part != 0 for p in plans) or any(p.kvh_sends for p in plans):
+            k_lo = self._buf("k_lo", (hk, lo, d), k.dtype)
+            v_lo = self._buf("v_lo", (hk, lo, d), v.dtype)
+            k_hi = self._buf("k_hi", (hk, rows - lo, d), k.dtype)
+            v_hi = self._buf("v_hi", (hk, rows - lo, d), v.dtype)
+            k_lo.copy_(k[:, :lo])
+            v_lo.copy_(v[:, :lo])
+            k_hi.copy_(k[:, lo:])
+            v_hi.copy_(v[:, lo:])
+            kvh_slot = (self._buf("kh_recv", (hk, rows - lo, d), k.dtype),
+                        self._buf("vh_recv", (hk, rows - lo, d), v.dtype))
 
         def post_operands(t):
             """sends of my immutable KV/Q for step t + the receive my step-t action needs."""
@@ -403,11 +427,17 @@ class DistRuntime:
                 sends += [(k, dst - 1), (v, dst - 1)]
                 self._sent(k, v)
                 rec.send(t, 0, w, dst, mk)
+            for dst in p.kvh_sends:
+                sends += [(k_hi, dst - 1), (v_hi, dst - 1)]
+                self._sent(k_hi, v_hi)
+                rec.send(t, 4, w, dst, mk)
             for dst in p.q_sends:
                 sends.append((q, dst - 1))
                 self._sent(q)
                 rec.send(t, 1, w, dst, mk)
-            if p.action == "direct":
+            if p.action == "direct" and p.part == KVPart.High:
+                recvs += [(kvh_slot[0], p.peer - 1), (kvh_slot[1], p.peer - 1)]
+            elif p.action == "direct":
                 ks, vs = kv_slot[t % 2]
                 recvs += [(ks, p.peer - 1), (vs, p.peer - 1)]
             elif p.action == "help":
@@ -426,7 +456,9 @@ class DistRuntime:
             cur_held = (1 if p.action in ("direct", "help") else 0) + (1 if nxt is not None and plans[t + 1].action in ("direct", "help") else 0)
             held = max(held, cur_held)
             m0 = rec.mark()
-            if p.action == "direct":
+            if p.action == "direct" and p.part == KVPart.High:
+                rec.arrive(t, 4, p.peer, w, m0, kvh_slot)
+            elif p.action == "direct":
                 rec.arrive(t, 0, p.peer, w, m0, kv_slot[t % 2])
             elif p.action == "help":
                 rec.arrive(t, 1, p.peer, w, m0, [q_slot[t % 2]])
@@ -435,14 +467,16 @@ class DistRuntime:
                 have_acc = True
                 rec.task("local_attn", m0, rec.mark())
             elif p.action == "direct":
-                ks, vs = kv_slot[t % 2]
+                ks, vs = kvh_slot if p.part == KVPart.High else kv_slot[t % 2]
                 be.update(q, ks, vs, acc if have_acc else None, "full", acc)
                 have_acc = True
-                rec.task(f"remote_attn q={w} kv={p.peer}", m0, rec.mark())
+                rec.task(f"remote_attn q={w} kv={p.peer}" +
+                         (" rows=high" if p.part == KVPart.High else ""), m0, rec.mark())
             elif p.action == "help":
                 if part_handle is not None:
                     part_handle.wait()  # the previous partial has left this buffer
-                be.update(q_slot[t % 2], k, v, None, "full", part)
+                kk, vv = (k_lo, v_lo) if p.part == KVPart.Low else (k, v)
+                be.update(q_slot[t % 2], kk, vv, None, "full", part)
                 m1 = rec.mark()
                 rec.task(f"helper_attn q={p.peer} kv={w}", m0, m1)
                 part_handle = tr.exchange([(part_pk, p.peer - 1)], [])
@@ -617,10 +651,12 @@ def bench_main(args) -> int:
     torch.manual_seed(1234 + rank)
     q, k, v, do = [(torch.rand(heads, rows, d, device=dev) * 2 - 1).to(torch.bfloat16) for _ in range(4)]
     rt = DistRuntime(rank, world, device=dev)
+    fwd_s = getattr(args, "fwd_schedule", "balanced")
+    bwd_s = getattr(args, "bwd_schedule", "balanced")
 
     def step():
-        rt.forward(q, k, v, "balanced")
-        rt.backward(do, "balanced")
+        rt.forward(q, k, v, fwd_s)
+        rt.backward(do, bwd_s)
 
     for _ in range(args.warmup):
         step()
@@ -643,7 +679,8 @@ def bench_main(args) -> int:
                 "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
                 "config": {"workload": f"llama7b-attn causal fwd+bwd, 32 heads, d=128, seq "
-                                       f"{n_total} over {world} B200 (balanced fwd + bwd, NCCL)",
+                                       f"{n_total} over {world} B200 ({fwd_s} fwd + {bwd_s} bwd, "
+                                       f"NCCL)",
                            "heads": heads, "d": d, "seq_len": n_total, "tokens_per_gpu": rows},
                 "tokens_per_s": n_total / (ms * 1e-3),
                 "tflops_per_gpu": fl / (ms * 1e-3) / 1e12 / world}

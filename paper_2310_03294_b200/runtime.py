@@ -182,7 +182,7 @@ def run_forward(shards: list[SequenceShard], schedule: Schedule | str = "balance
     """runtime.cpp:491-529: runs the schedule's forward over all P workers on
     this device; writes out (bf16) / lse (fp32) into the shards."""
     kind = schedule if isinstance(schedule, str) else _schedule_kind(schedule)
-    kind_i = {"ring": 0, "balanced": 1}[kind]
+    kind_i = {"ring": 0, "balanced": 1, "balanced_split": 4}[kind]
     for s in shards:
         h, rows, d = s.q.shape
         if s.out is None:
@@ -227,13 +227,16 @@ def run_backward(shards: list[SequenceShard], schedule: str = "ring",
 
 
 def _schedule_kind(s: Schedule) -> str:
-    from .schedule import build_balanced_schedule, build_ring_schedule, validate
+    from .schedule import (build_balanced_schedule, build_balanced_split_schedule,
+                           build_ring_schedule, validate)
     from .errors import ScheduleError
     v = validate(s)
     if v:
         raise ScheduleError(f"invalid schedule: {v[0]} ({len(v)} violations)")
-    for name, b in (("ring", build_ring_schedule), ("balanced", build_balanced_schedule)):
+    for name, b in (("ring", build_ring_schedule), ("balanced", build_balanced_schedule),
+                    ("balanced_split", build_balanced_split_schedule)):
         ref = b(s.workers)
         if ref.flat() == s.flat():
             return name
-    raise ScheduleError("the device executor runs the ring and balanced schedules only")
+    raise ScheduleError("the device executor runs the ring, balanced and balanced_split "
+                        "schedules only")

@@ -28,10 +28,19 @@ class PayloadKind(enum.IntEnum):
     Q = 1
     PartialResult = 2
     GradKV = 3
+    KVHalf = 4  # split-schedule extension: half of a kv chunk's rows
+
+
+class KVPart(enum.IntEnum):
+    """Rows of the kv chunk a RemoteAttn task covers (split extension; carried
+    in Task.helper, which the reference only uses for RescaleMerge)."""
+    Whole = 0
+    Low = 1    # rows [0, c/2)
+    High = 2   # rows [c/2, c)
 
 
 _TASK_NAMES = {0: "local_attn", 1: "remote_attn", 2: "rescale_merge", 3: "idle"}
-_PAYLOAD_NAMES = {0: "kv", 1: "q", 2: "partial", 3: "grad_kv"}
+_PAYLOAD_NAMES = {0: "kv", 1: "q", 2: "partial", 3: "grad_kv", 4: "kv_half"}
 
 
 @dataclass(frozen=True)
@@ -44,6 +53,16 @@ class Task:
 
     def is_attention(self) -> bool:
         return self.kind in (TaskKind.LocalAttn, TaskKind.RemoteAttn)
+
+    @property
+    def kv_part(self) -> KVPart:
+        return KVPart(self.helper) if self.kind == TaskKind.RemoteAttn else KVPart.Whole
+
+    def weight(self) -> Fraction:
+        """Chunk pairs of work: 1, or 1/2 for a split-step half task."""
+        if not self.is_attention():
+            return Fraction(0)
+        return Fraction(1) if self.kv_part == KVPart.Whole else Fraction(1, 2)
 
 
 @dataclass(frozen=True)
@@ -117,6 +136,14 @@ def build_balanced_schedule(workers: int) -> Schedule:
     return _build(workers, 1)
 
 
+def build_balanced_split_schedule(workers: int) -> Schedule:
+    """Balanced forward with the even-P last step split (extension, SURVEY
+    §8(f)2; DA_SCHEDULE_BALANCED_SPLIT). At t = P/2 helper p computes pair
+    (p + P/2, p) on the low half of its kv rows (Q in, Partial out) and the
+    owner on the high half (KVHalf in). Odd P: the balanced schedule."""
+    return _build(workers, 4)
+
+
 def build_ring_backward_schedule(workers: int) -> Schedule:
     """The reference run_backward order (runtime.cpp:605-651) as an explicit
     schedule: the ring task table plus a GradKV message per direct pair."""
@@ -161,6 +188,27 @@ def expected_speedup(s: Schedule) -> Fraction:
     return Fraction(0) if s.step_count() == 0 else Fraction(s.attention_task_count(), s.step_count())
 
 
+def weighted_makespan(s: Schedule, diag_weight: Fraction = Fraction(1)) -> Fraction:
+    """Sum over steps of the heaviest primary task (chunk-pair units; half
+    tasks weigh 1/2, the causal diagonal `diag_weight`)."""
+    total = Fraction(0)
+    for step in s.steps:
+        w = [diag_weight if t.kind == TaskKind.LocalAttn else t.weight() for t in step]
+        total += max(w, default=Fraction(0))
+    return total
+
+
+def weighted_speedup(s: Schedule, diag_weight: Fraction = Fraction(1)) -> Fraction:
+    """Ideal speedup over one worker doing all pairs, counting work instead of
+    tasks: with diag_weight = 1/2 (causal diagonal costs half a pair) this is
+    the FLOP-level ceiling (P=8: ring 64/15, balanced 64/9, balanced_split 8;
+    split over ring 1.875x vs balanced over ring 5/3)."""
+    work = sum((diag_weight if t.kind == TaskKind.LocalAttn else t.weight())
+               for st in s.steps for t in st)
+    ms = weighted_makespan(s, diag_weight)
+    return Fraction(0) if ms == 0 else work / ms
+
+
 def ring_idle_fraction_formula(workers: int) -> Fraction:
     if workers < 1:
         raise ConfigError("need at least 1 worker")
@@ -180,6 +228,8 @@ def schedule_to_json(s: Schedule) -> str:
         if t.kind == TaskKind.RemoteAttn:
             j["query_owner"] = t.query_owner
             j["kv_owner"] = t.kv_owner
+            if t.kv_part != KVPart.Whole:
+                j["kv_part"] = t.kv_part.name.lower()
         elif t.kind == TaskKind.RescaleMerge:
             j["helper"] = t.helper
         return j

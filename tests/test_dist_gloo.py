@@ -116,7 +116,9 @@ def _worker(rank, world, port, n, d, heads, schedule, bwd_schedule, outdir):
 
 @pytest.mark.parametrize("world,schedule,bwd", [(2, "balanced", "ring"), (3, "balanced", "balanced"),
                                                 (4, "balanced", "balanced"), (4, "ring", "ring"),
-                                                (5, "balanced", "balanced")])
+                                                (5, "balanced", "balanced"),
+                                                (2, "balanced_split", "ring"),
+                                                (4, "balanced_split", "balanced")])
 def test_dist_runtime_gloo_bit_exact(world, schedule, bwd):
     n, d, heads = 16 * world, 8, 2
     with tempfile.TemporaryDirectory() as td:

@@ -147,3 +147,17 @@ def test_ring_and_balanced_agree_and_state_errors(cuda):
     c = make_parity_shards(5, 2, 256, 1, 128)
     with pytest.raises(StateError):
         run_backward(c)
+
+
+@pytest.mark.parametrize("P,n,heads,heads_kv", [(4, 4096, 1, 1), (2, 1024, 1, 1), (8, 2048, 2, 2),
+                                                (6, 1500, 1, 1), (4, 1024, 4, 2)])
+def test_balanced_split_forward(cuda, P, n, heads, heads_kv):
+    """Even-P last-step split (extension): half-pair tasks on packed kv row
+    halves, the same results as the oracle stepper running the same table;
+    counters equal (H=1) — half KV messages are counted at their size."""
+    from paper_2310_03294_b200.runtime import make_parity_shards, run_backward, run_forward
+    shards = make_parity_shards(5, P, n, heads, 128, heads_kv=heads_kv)
+    tf = run_forward(shards, "balanced_split")
+    tb = run_backward(shards)
+    torch.cuda.synchronize()
+    _check_against_oracle(shards, P, n, "balanced_split", heads, tf, tb, heads_kv=heads_kv)
