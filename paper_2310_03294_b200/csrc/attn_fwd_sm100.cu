@@ -103,15 +103,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n_q_tiles = (p.rows_q + kBM - 1) / kBM;
   const int n_kv_tiles = (p.rows_kv + kBN - 1) / kBN;
   const int n_pairs = (n_q_tiles + 1) / 2;
-#ifdef DA_HEAD_MINOR_GRID
-  const int head = blockIdx.x % p.h_q;
-  const int pair = n_pairs - 1 - static_cast<int>(blockIdx.x / p.h_q);
-#else
   // head-major: the co-resident CTAs share one head's K/V in L2; within a
   // head the heaviest (latest) query pairs launch first
   const int head = static_cast<int>(blockIdx.x / n_pairs);
   const int pair = n_pairs - 1 - static_cast<int>(blockIdx.x % n_pairs);
-#endif
   const int kv_head = head / (p.h_q / p.h_kv);
   const int qt0 = 2 * pair;
   const bool has_t1 = (qt0 + 1) < n_q_tiles;
