@@ -28,7 +28,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define DA_ABI_VERSION 1
+#define DA_ABI_VERSION 2
 
 typedef enum da_status {
   DA_OK = 0,
@@ -136,6 +136,11 @@ typedef struct da_bwd_args {
   int accumulate_kv;
   float scale;
   int mask;
+  /* deterministic != 0: the fp32 dq partials of the kv tiles are added in a
+   * fixed order (descending kv tile, enforced by per-(head, q tile)
+   * semaphores), so dq_acc is bitwise reproducible run to run. Default 0 is
+   * the faster unordered reduction (results agree to fp32 rounding). */
+  int deterministic;
 } da_bwd_args;
 
 da_status da_attn_bwd_chunk(const da_bwd_args* args, void* stream);

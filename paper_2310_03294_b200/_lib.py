@@ -27,7 +27,8 @@ class BwdArgs(C.Structure):
     _fields_ = [("q", vp), ("k", vp), ("v", vp), ("d_out", vp), ("lse", vp), ("d_vec", vp),
                 ("h_q", i64), ("h_kv", i64), ("rows_q", i64), ("rows_kv", i64), ("d", i64),
                 ("dq_acc", vp), ("dk_acc", vp), ("dv_acc", vp),
-                ("accumulate_kv", C.c_int), ("scale", f32), ("mask", C.c_int)]
+                ("accumulate_kv", C.c_int), ("scale", f32), ("mask", C.c_int),
+                ("deterministic", C.c_int)]
 
 
 class Shards(C.Structure):

@@ -101,7 +101,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n_q_tiles = (p.rows_q + kBM - 1) / kBM;
   const int n_kv_tiles = (p.rows_kv + kBN - 1) / kBN;
   const int kv_head = static_cast<int>(blockIdx.x / n_kv_tiles);
-  const int jt = static_cast<int>(blockIdx.x % n_kv_tiles);
+  // deterministic mode launches each head's kv tiles lightest-first: a CTA
+  // only ever waits for a higher kv tile, which was launched before it
+  const int jt = p.dq_sem != nullptr ? n_kv_tiles - 1 - static_cast<int>(blockIdx.x % n_kv_tiles)
+                                     : static_cast<int>(blockIdx.x % n_kv_tiles);
   const int group = p.h_q / p.h_kv;
   const int i0 = (p.mask == DA_MASK_DIAGONAL) ? jt : 0;
   const int n_i = n_q_tiles - i0;
@@ -310,6 +313,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&bars->dq_drained);
+      // deterministic order: the partials of query tile (hq, qt) are added by
+      // descending kv tile; wait until every higher contributor has landed
+      int* sem = nullptr;
+      if (p.dq_sem != nullptr) {
+        sem = p.dq_sem + static_cast<size_t>(hq) * n_q_tiles + cur.qt;
+        const int turn = (p.mask == DA_MASK_DIAGONAL ? cur.qt : n_kv_tiles - 1) - jt;
+        if (dw == 0 && lane == 0) {
+          while (ld_acquire_gpu(sem) != turn) __nanosleep(64);
+        }
+        named_bar_sync(1, 128);
+        fence_proxy_async_global();
+      }
       // stage [32 q][32 d] boxes (this warp's 32 head-dim columns) and let TMA
       // reduce them into dq_acc: no LSU atomics; OOB query rows are clipped
       float* box = reinterpret_cast<float*>(smem + SmemLayout::dq_stage) + dw * 32 * 32;
@@ -324,6 +339,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
           tma_reduce_add_3d(&tmap_dq, box, dw * 32, row0 + c * 32, hq);
           bulk_commit();
+        }
+      }
+      if (sem != nullptr) {
+        // this CTA's partial is complete in global memory: pass the turn on
+        if (lane == 0) bulk_wait<0>();
+        __syncwarp();
+        fence_proxy_async_global();
+        named_bar_sync(1, 128);
+        if (dw == 0 && lane == 0) {
+          __threadfence();
+          red_release_gpu_add(sem, 1);
         }
       }
     }

@@ -81,6 +81,27 @@ da_status make_tmap_f32_acc(CUtensorMap* map, void* base, int64_t heads, int64_t
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 unsigned long long* g_bwd_trace = nullptr;
+
+// Semaphores of the deterministic dQ order: one int per (query head, query
+// tile), zeroed before every deterministic launch. Grown on demand, cached
+// per thread (allocation happens once per shape, not per call).
+struct SemBuffer {
+  int* ptr = nullptr;
+  size_t n = 0;
+  ~SemBuffer() {
+    if (ptr) cudaFree(ptr);
+  }
+  cudaError_t ensure(size_t want) {
+    if (want <= n) return cudaSuccess;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&ptr, want * sizeof(int));
+    if (e == cudaSuccess) n = want;
+    return e;
+  }
+};
+thread_local SemBuffer g_dq_sem;
 unsigned long long* g_fwd_trace = nullptr;
 
 }  // namespace da
@@ -269,6 +290,14 @@ da_status da_attn_bwd_chunk(const da_bwd_args* a, void* stream) {
   p.dq_acc = a->dq_acc;
   p.dk_acc = a->dk_acc;
   p.dv_acc = a->dv_acc;
+  p.dq_sem = nullptr;
+  if (a->deterministic) {
+    const size_t n_sem = static_cast<size_t>(a->h_q) * ((a->rows_q + 127) / 128);
+    cudaError_t e = da::g_dq_sem.ensure(n_sem);
+    if (e == cudaSuccess) e = cudaMemsetAsync(da::g_dq_sem.ptr, 0, n_sem * sizeof(int), st);
+    if (e != cudaSuccess) return da::cuda_error(e, "block_attn_backward deterministic workspace");
+    p.dq_sem = da::g_dq_sem.ptr;
+  }
   p.trace = da::g_bwd_trace;
   cudaError_t e = da::launch_attn_bwd(tq, tk, tv, tdo, tdq, p, st);
   return e == cudaSuccess ? DA_OK : da::cuda_error(e, "da_attn_bwd_chunk launch");

@@ -38,6 +38,7 @@ struct BwdParams {
   float* dq_acc;
   float* dk_acc;
   float* dv_acc;
+  int* dq_sem;  // deterministic mode: [h_q, q tiles] zeroed counters, else nullptr
   unsigned long long* trace;  // DA_TRACE builds: per-iteration clock64 stamps of CTA 0
 };
 

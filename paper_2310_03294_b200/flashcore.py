@@ -180,12 +180,14 @@ def backward_aux(d_out: torch.Tensor, out: torch.Tensor, stream=None) -> torch.T
 
 def block_attn_backward(q, k, v, out, lse, d_out, mask: MaskMode, scale: float | None = None, *,
                         d_vec: torch.Tensor | None = None, grads: ChunkGrads | None = None,
-                        accumulate_kv: bool = False, stream=None) -> ChunkGrads:
+                        accumulate_kv: bool = False, deterministic: bool = False,
+                        stream=None) -> ChunkGrads:
     """flashcore.hpp:269-337: gradient contributions of one (query chunk, kv chunk) pair.
 
     Returns fp32 ChunkGrads. With `grads` given, dq is accumulated into grads.dq and
     dk/dv are added (accumulate_kv) or overwritten. `d_vec` (backward_aux) is
-    computed when not supplied.
+    computed when not supplied. deterministic=True adds the dq partials in a
+    fixed order (bitwise reproducible; dk/dv always are).
     """
     for t, n in ((q, "q"), (k, "k"), (v, "v"), (d_out, "d_out")):
         _req(t, torch.bfloat16, n)
@@ -207,5 +209,6 @@ def block_attn_backward(q, k, v, out, lse, d_out, mask: MaskMode, scale: float |
     a.accumulate_kv = 1 if accumulate_kv else 0
     a.scale = float(scale) if scale is not None else 0.0
     a.mask = int(mask)
+    a.deterministic = 1 if deterministic else 0
     check(_lib.lib().da_attn_bwd_chunk(C.byref(a), _stream(stream)))
     return grads

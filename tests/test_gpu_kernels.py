@@ -168,3 +168,34 @@ def test_host_pipeline_degenerate_rows_raise(cuda):
                               F.MaskMode.Full, degenerate_flag=flag)
     with pytest.raises(DegenerateRowError):
         F.check_degenerate(flag)
+
+
+@pytest.mark.parametrize("h,hkv,n,diag", [(2, 2, 1024, True), (4, 2, 640, True), (2, 2, 384, False),
+                                          (1, 1, 40000, True)])
+def test_bwd_deterministic_dq_is_bitwise_reproducible(cuda, h, hkv, n, diag):
+    """deterministic=True orders the fp32 dq partials (descending kv tile), so
+    repeated launches give identical bits; the values match the default
+    (unordered) reduction to fp32 rounding and the fp32 reference."""
+    from paper_2310_03294_b200.flashcore import MaskMode, block_attn_backward
+    q, k, v = _qkv(h, n, hkv, seed=7 + n)
+    d_out = _qkv(h, n, hkv, seed=8 + n)[0]
+    mask = MaskMode.Diagonal if diag else MaskMode.Full
+    if n <= 2048:
+        o_ref, lse_ref = attention_ref(q, k, v, diag)
+    else:  # long single head: the kernel's own forward supplies O / LSE
+        from paper_2310_03294_b200.flashcore import block_attn_update_final
+        fo = block_attn_update_final(q, k, v, None, mask)
+        o_ref, lse_ref = fo.o.float(), fo.lse
+    out_bf = o_ref.to(torch.bfloat16)
+    runs = [block_attn_backward(q, k, v, out_bf, lse_ref.contiguous(), d_out, mask,
+                                deterministic=True) for _ in range(3)]
+    fast = block_attn_backward(q, k, v, out_bf, lse_ref.contiguous(), d_out, mask)
+    torch.cuda.synchronize()
+    for g in runs[1:]:
+        assert torch.equal(g.dq, runs[0].dq) and torch.equal(g.dk, runs[0].dk) and \
+            torch.equal(g.dv, runs[0].dv)
+    assert rel_err(runs[0].dq, fast.dq) < 1e-5
+    assert torch.equal(runs[0].dk, fast.dk) and torch.equal(runs[0].dv, fast.dv)
+    if n <= 2048:
+        dq, dk, dv = attention_grads_ref(q, k, v, d_out, diag)
+        assert rel_err(runs[0].dq, dq) < TOL

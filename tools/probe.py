@@ -42,6 +42,13 @@ def main():
         block_attn_backward(q, k, v, out.o, out.lse, d_out, MaskMode.Diagonal, d_vec=dvec, grads=grads)
     t_bwd = timeit(bwd)
     print(f"bwd  H={h} N={n}: {t_bwd:.3f} ms  {fl_bwd / t_bwd / 1e9:.1f} TFLOP/s", flush=True)
+
+    def bwd_det():
+        block_attn_backward(q, k, v, out.o, out.lse, d_out, MaskMode.Diagonal, d_vec=dvec, grads=grads,
+                            deterministic=True)
+    t_det = timeit(bwd_det)
+    print(f"bwd (deterministic dq) H={h} N={n}: {t_det:.3f} ms  {fl_bwd / t_det / 1e9:.1f} TFLOP/s",
+          flush=True)
     print(f"fwd+bwd: {t_fwd + t_bwd:.3f} ms  {(fl_fwd + fl_bwd) / (t_fwd + t_bwd) / 1e9:.1f} TFLOP/s")
 
 
