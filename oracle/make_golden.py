@@ -9,6 +9,8 @@ Fixtures (all produced by the reference's own code, run here):
                       reference acceptance grid shapes (P x N x d, seed 0)
   numerics_d128.npz   bf16-rounded inputs, N=512, P=4, d=128, balanced, float32
                       outputs (the GPU-shape fixture)
+  ckpt.json           checkpoint plans (ckptplan.cpp): positions, recompute counts,
+                      cost-model times, saved scalars for L = 1..3
 """
 from __future__ import annotations
 
@@ -34,6 +36,7 @@ def main():
     OUT.mkdir(parents=True, exist_ok=True)
     (OUT / "rng.json").write_text(json.dumps(O.ref_json("rng"), indent=1) + "\n")
     (OUT / "schedules.json").write_text(json.dumps(O.ref_json("schedules")) + "\n")
+    (OUT / "ckpt.json").write_text(json.dumps(O.ref_json("ckpt"), indent=0) + "\n")
 
     arrays, meta = {}, {}
     for P, N, d, sched in SMALL_GRID:

@@ -8,6 +8,9 @@
 //        runs make_shards/run_forward/run_backward (reference executors),
 //        writes q,k,v,d_out,out,lse,dq,dk,dv as float64 [H][N][D] binaries
 //        plus counters/trace JSON. bf16=1 rounds q/k/v/d_out to bf16 first.
+//   ref_driver ckpt                           -> JSON: checkpoint plans (ckptplan.cpp):
+//        positions, recompute counts of run_with_checkpointing on a small
+//        pipeline, cost-model times, saved scalars, cross-plan bitwise flags
 //   ref_driver time N P H D SCHED THREADS
 //        wall time of forward+backward with the reference's concurrent
 //        executor (P threads per head; heads spread over THREADS/P workers).
@@ -26,6 +29,7 @@
 #include <thread>
 #include <vector>
 
+#include "distattn/ckptplan.hpp"
 #include "distattn/flashcore.hpp"
 #include "distattn/numerics.hpp"
 #include "distattn/runtime.hpp"
@@ -122,6 +126,48 @@ int main(int argc, char** argv) {
         dump_schedule(std::cout, da::build_balanced_schedule(P));
       }
       std::cout << "]}\n";
+      return 0;
+    }
+    if (mode == "ckpt") {
+      const da::CheckpointStrategy strats[3] = {da::CheckpointStrategy::None,
+                                                 da::CheckpointStrategy::LayerBoundary,
+                                                 da::CheckpointStrategy::AttentionOutput};
+      const da::CkptCostModel cost{3.0, 5.0, 11.0};
+      std::cout << "{\"cases\":[";
+      bool first = true;
+      for (int L = 1; L <= 3; ++L) {
+        const da::LayerPipeline pipe = da::make_pipeline(L, 12, 4, 8, 7);
+        da::Rng r(11);
+        const da::Matd x = r.matrix(12, 4, -1.0, 1.0);
+        const da::Matd g = r.matrix(12, 4, -1.0, 1.0);
+        std::vector<da::CkptRunResult> runs;
+        for (const auto st : strats) {
+          const da::CheckpointPlan pl = da::plan(pipe, st);
+          runs.push_back(da::run_with_checkpointing(pipe, pl, x, g));
+          const auto& tr = runs.back().trace;
+          std::cout << (first ? "" : ",") << "{\"layers\":" << L << ",\"strategy\":\""
+                    << da::to_string(st) << "\",\"positions\":[";
+          for (size_t i = 0; i < pl.saved_positions.size(); ++i)
+            std::cout << (i ? "," : "") << pl.saved_positions[i];
+          std::cout << "],\"counts\":[";
+          for (int k = 0; k < da::kOpsPerLayer; ++k) std::cout << (k ? "," : "") << tr.counts[k];
+          std::cout << "],\"iteration_time\":" << da::iteration_time_model(cost, L, st)
+                    << ",\"recompute_time\":" << da::recompute_time(tr, cost)
+                    << ",\"saved_activation_scalars\":" << da::saved_activation_scalars(pl, pipe)
+                    << "}";
+          first = false;
+        }
+        // the reference's bitwise cross-plan property (ckptplan.hpp:8-9)
+        for (size_t i = 1; i < runs.size(); ++i) {
+          const auto& a = runs[0].grads;
+          const auto& b = runs[i].grads;
+          bool same = true;
+          for (da::Index j = 0; j < a.d_input.size(); ++j)
+            same = same && a.d_input.data()[j] == b.d_input.data()[j];
+          if (!same) throw std::runtime_error("reference cross-plan grads differ");
+        }
+      }
+      std::cout << "],\"cost\":[3.0,5.0,11.0]}\n";
       return 0;
     }
     if (mode == "rng") {
