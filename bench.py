@@ -273,7 +273,7 @@ def run_single(args):
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
                 "path": "pipeline.HostAttention (flashcore.block_attn_update_final + backward_aux + "
                         "block_attn_backward over the C ABI): pinned-host q/k/v/dO in, bf16 "
-                        "dQ/dK/dV out, copies overlapped per group of %d heads" % args.heads_per_group},
+                        "dQ/dK/dV out, copies overlapped per group of %d heads, 2 compute streams" % args.heads_per_group},
         "gpu_launches": 3 * args.steps,
         "clocks": clk.summary(),
     }
@@ -303,7 +303,7 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seq", type=int, default=SEQ)
     ap.add_argument("--heads", type=int, default=H)
-    ap.add_argument("--heads-per-group", type=int, default=2)
+    ap.add_argument("--heads-per-group", type=int, default=1)
     ap.add_argument("--fwd-schedule", default="balanced", choices=["ring", "balanced", "balanced_split"])
     ap.add_argument("--bwd-schedule", default="balanced", choices=["ring", "balanced"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -32,7 +32,7 @@ class HostAttention:
     """
 
     def __init__(self, heads: int, rows: int, d: int = 128, heads_per_group: int = 4,
-                 device="cuda"):
+                 device="cuda", compute_streams: int = 2):
         if heads % heads_per_group != 0:
             raise ShapeError(f"heads ({heads}) must be a multiple of heads_per_group "
                              f"({heads_per_group})")
@@ -48,6 +48,9 @@ class HostAttention:
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
         self.h2d = torch.cuda.Stream(dev)
         self.d2h = torch.cuda.Stream(dev)
+        # groups alternate between compute streams so one group's backward tail
+        # overlaps the next group's forward (fills the wave-quantisation gaps)
+        self.comp = [torch.cuda.Stream(dev) for _ in range(max(1, compute_streams))]
         self.out = None
         self.lse = None
 
@@ -73,13 +76,15 @@ class HostAttention:
             if t.shape != (self.heads, self.rows, self.d) or t.dtype != torch.bfloat16:
                 raise ShapeError("HostAttention: host tensors must be bf16 "
                                  f"[{self.heads}, {self.rows}, {self.d}]")
-        comp = torch.cuda.current_stream()
+        cur = torch.cuda.current_stream()
         self.flag.zero_()
         n_groups = self.heads // self.hg
         in_ready = [torch.cuda.Event() for _ in range(n_groups)]
         out_ready = [torch.cuda.Event() for _ in range(n_groups)]
-        # the previous call's readers of the device buffers are on `comp`
-        self.h2d.wait_stream(comp)
+        # the previous call's readers of the device buffers finished on `cur`
+        self.h2d.wait_stream(cur)
+        for c in self.comp:
+            c.wait_stream(cur)
         with torch.cuda.stream(self.h2d):
             for g in range(n_groups):
                 sl = slice(g * self.hg, (g + 1) * self.hg)
@@ -89,17 +94,19 @@ class HostAttention:
         outs, lses = [], []
         for g in range(n_groups):
             sl = slice(g * self.hg, (g + 1) * self.hg)
+            comp = self.comp[g % len(self.comp)]
             comp.wait_event(in_ready[g])
-            q, k, v, do = self.q[sl], self.k[sl], self.v[sl], self.d_out[sl]
-            out = F.block_attn_update_final(q, k, v, None, F.MaskMode.Diagonal, stream=comp,
-                                            degenerate_flag=self.flag)
-            dvec = F.backward_aux(do, out.o, stream=comp)
-            grads = F.ChunkGrads(self.dq[sl], self.dk[sl], self.dv[sl])
-            grads.dq.zero_()
-            F.block_attn_backward(q, k, v, out.o, out.lse, do, F.MaskMode.Diagonal, d_vec=dvec,
-                                  grads=grads, stream=comp)
-            for src, dst in ((self.dq, self.dq16), (self.dk, self.dk16), (self.dv, self.dv16)):
-                self._convert(src[sl], dst[sl], comp)
+            with torch.cuda.stream(comp):
+                q, k, v, do = self.q[sl], self.k[sl], self.v[sl], self.d_out[sl]
+                out = F.block_attn_update_final(q, k, v, None, F.MaskMode.Diagonal, stream=comp,
+                                                degenerate_flag=self.flag)
+                dvec = F.backward_aux(do, out.o, stream=comp)
+                grads = F.ChunkGrads(self.dq[sl], self.dk[sl], self.dv[sl])
+                grads.dq.zero_()
+                F.block_attn_backward(q, k, v, out.o, out.lse, do, F.MaskMode.Diagonal,
+                                      d_vec=dvec, grads=grads, stream=comp)
+                for src, dst in ((self.dq, self.dq16), (self.dk, self.dk16), (self.dv, self.dv16)):
+                    self._convert(src[sl], dst[sl], comp)
             out_ready[g].record(comp)
             self.d2h.wait_event(out_ready[g])
             with torch.cuda.stream(self.d2h):
@@ -107,7 +114,10 @@ class HostAttention:
                     dst[sl].copy_(src[sl], non_blocking=True)
             outs.append(out.o)
             lses.append(out.lse)
-        comp.wait_stream(self.d2h)
+        cur.wait_stream(self.d2h)
+        for c in self.comp:
+            cur.wait_stream(c)
+        comp = cur
         self.out, self.lse = outs, lses  # the rematerialisation state (saved O, LSE) per group
         if sync:
             F.check_degenerate(self.flag, stream=comp)

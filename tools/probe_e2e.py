@@ -11,8 +11,9 @@ h, n = 32, int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 host = [(torch.rand(h, n, 128) * 2 - 1).to(torch.bfloat16).pin_memory() for _ in range(4)]
 outs = [torch.empty(h, n, 128, dtype=torch.bfloat16).pin_memory() for _ in range(3)]
 fl = 7 * n * n * 128 * h
-for hpg in [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "1,2,4,8,16,32").split(",")]:
-    ha = HostAttention(h, n, 128, heads_per_group=hpg)
+for spec in (sys.argv[2] if len(sys.argv) > 2 else "2x1,2x2,4x2").split(","):
+    hpg, cs = (int(x) for x in spec.split("x"))
+    ha = HostAttention(h, n, 128, heads_per_group=hpg, compute_streams=cs)
     for _ in range(2):
         ha(*host, *outs)
     torch.cuda.synchronize()
@@ -23,6 +24,6 @@ for hpg in [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "1,2,4,8,16,3
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / 4
-    print(f"hpg {hpg:2d}: {ms:.2f} ms  {fl / ms / 1e9:.1f} TFLOP/s e2e", flush=True)
+    print(f"hpg {hpg:2d} streams {cs}: {ms:.2f} ms  {fl / ms / 1e9:.1f} TFLOP/s e2e", flush=True)
     del ha
     torch.cuda.empty_cache()
