@@ -199,11 +199,11 @@ def run_single(args):
             ev["bwd"].append((e[2], e[3]))
         return out
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(0) as clk:
+    with ClockSampler(0) as clk:  # started before the warm-up: nvidia-smi needs ~0.2 s
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
         start.record(stream)
         for _ in range(args.steps):
             step(record=True)
@@ -307,13 +307,15 @@ def main(argv=None):
     ap.add_argument("--fwd-schedule", default="balanced", choices=["ring", "balanced", "balanced_split"])
     ap.add_argument("--bwd-schedule", default="balanced", choices=["ring", "balanced"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the torchrun/NCCL path even at one rank (tests the N>1 code)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if args.gpus > 1 or world > 1:
+    if args.gpus > 1 or world > 1 or args.force_dist:
         return run_multi(args)
     return run_single(args)
 

@@ -633,11 +633,13 @@ class DistRuntime:
 # ----------------------------------------------------------------------------- bench (N > 1)
 def bench_main(args) -> int:
     """torchrun entry for bench.py --gpus N: sequence-parallel fwd+bwd of the
-    Llama-7B attention layer at seq 32K x N (32K tokens per GPU, weak scaling),
-    balanced forward + balanced backward over NCCL."""
+    Llama-7B attention layer at seq 32K x N (32K tokens per GPU, weak scaling)
+    over NCCL. Device-timed steps (barrier + synchronize on both sides, max over
+    ranks), then an e2e pass that copies each rank's q/k/v/dO shard in from
+    pinned host memory and its bf16 dq/dk/dv out inside the timed region."""
     import json
-    import statistics
-    import time
+    import sys as _sys
+    from pathlib import Path
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -656,34 +658,97 @@ def bench_main(args) -> int:
 
     def step():
         rt.forward(q, k, v, fwd_s)
-        rt.backward(do, bwd_s)
+        return rt.backward(do, bwd_s)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    tdist.barrier()
+    root = Path(__file__).resolve().parents[1]
+    if str(root) not in _sys.path:
+        _sys.path.insert(0, str(root))
+    from bench import ClockSampler, peaks  # noqa: E402  (same sampler as the N=1 arm)
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for _ in range(args.steps):
-        step()
-    e.record()
-    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:  # started before the warm-up: nvidia-smi needs ~0.2 s
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        tdist.barrier()
+        s.record()
+        for _ in range(args.steps):
+            step()
+        e.record()
+        torch.cuda.synchronize()
     tdist.barrier()
     ms = torch.tensor([s.elapsed_time(e) / args.steps], device=dev)
     tdist.all_reduce(ms, op=tdist.ReduceOp.MAX)
     ms = ms.item()
+
+    # e2e through the same public API with host buffers
+    host_in = [t.cpu().pin_memory() for t in (q, k, v, do)]
+    host_out = [torch.empty(heads, rows, d, dtype=torch.bfloat16).pin_memory() for _ in range(3)]
+    dev_in = [torch.empty_like(t) for t in (q, k, v, do)]
+
+    def e2e_step():
+        for dst, src in zip(dev_in, host_in):
+            dst.copy_(src, non_blocking=True)
+        rt.forward(dev_in[0], dev_in[1], dev_in[2], fwd_s)
+        grads = rt.backward(dev_in[3], bwd_s)
+        for src, dst in zip(grads, host_out):
+            dst.copy_(src.to(torch.bfloat16), non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    tdist.barrier()
+    e_steps = max(2, min(args.steps, 5))
+    s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s2.record()
+    for _ in range(e_steps):
+        e2e_step()
+    e2.record()
+    torch.cuda.synchronize()
+    tdist.barrier()
+    ms_e2e = torch.tensor([s2.elapsed_time(e2) / e_steps], device=dev)
+    tdist.all_reduce(ms_e2e, op=tdist.ReduceOp.MAX)
+    ms_e2e = ms_e2e.item()
     fl = 7.0 * n_total * n_total * d * heads
+    peak, peak_sus, src = peaks()
+    per_gpu = fl / (ms * 1e-3) / 1e12 / world
+    # kernel launches per rank per step: one attention launch per task, a merge
+    # per received partial, finalize, preprocess + one backward launch per task
+    sched_f = {"balanced": build_balanced_schedule, "ring": build_ring_schedule,
+               "balanced_split": build_balanced_split_schedule}[fwd_s](world)
+    launches = 0
+    for st in sched_f.steps:
+        for t in st:
+            if t.kind in (TaskKind.LocalAttn, TaskKind.RemoteAttn, TaskKind.RescaleMerge):
+                launches += 1
+    sched_b = (build_balanced_backward_schedule if bwd_s == "balanced"
+               else build_ring_backward_schedule)(world)
+    for st in sched_b.steps:
+        for t in st:
+            if t.kind in (TaskKind.LocalAttn, TaskKind.RemoteAttn):
+                launches += 1
+    launches += 2 * world  # finalize + backward preprocess per rank
     if rank == 0:
         line = {"metric": "attn fwd+bwd TFLOP/s", "value": fl / (ms * 1e-3) / 1e12,
                 "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-                "config": {"workload": f"llama7b-attn causal fwd+bwd, 32 heads, d=128, seq "
+                "config": {"workload": f"llama7b-attn causal fwd+bwd, {heads} heads, d=128, seq "
                                        f"{n_total} over {world} B200 ({fwd_s} fwd + {bwd_s} bwd, "
                                        f"NCCL)",
-                           "heads": heads, "d": d, "seq_len": n_total, "tokens_per_gpu": rows},
+                           "heads": heads, "d": d, "seq_len": n_total, "tokens_per_gpu": rows,
+                           "l2": "inputs exceed L2; no flush"},
                 "tokens_per_s": n_total / (ms * 1e-3),
-                "tflops_per_gpu": fl / (ms * 1e-3) / 1e12 / world}
+                "tflops_per_gpu": per_gpu,
+                "roofline": {"bound": "tensor", "kernel": "whole step per GPU (compute + exposed "
+                             "NVLink)", "achieved": per_gpu, "peak": peak, "unit": "TFLOP/s",
+                             "frac": per_gpu / peak, "peak_source": src, "traffic": None},
+                "e2e": {"value": fl / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s",
+                        "h2d_bytes_per_step": 4 * heads * n_total * d * 2,
+                        "d2h_bytes_per_step": 3 * heads * n_total * d * 2,
+                        "ms_per_step": ms_e2e,
+                        "path": "dist.DistRuntime forward/backward with pinned-host shards in "
+                                "and bf16 grads out, every rank"},
+                "gpu_launches": launches * args.steps,
+                "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     tdist.destroy_process_group()
     return 0

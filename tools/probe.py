@@ -26,18 +26,20 @@ def timeit(fn, iters=5, warm=2):
 def main():
     h = int(sys.argv[1]) if len(sys.argv) > 1 else 32
     n = int(sys.argv[2]) if len(sys.argv) > 2 else 32768
+    hkv = int(sys.argv[3]) if len(sys.argv) > 3 else h
     torch.manual_seed(0)
-    q, k, v = [(torch.rand(h, n, 128, device="cuda") * 2 - 1).to(torch.bfloat16) for _ in range(3)]
+    q = (torch.rand(h, n, 128, device="cuda") * 2 - 1).to(torch.bfloat16)
+    k, v = [(torch.rand(hkv, n, 128, device="cuda") * 2 - 1).to(torch.bfloat16) for _ in range(2)]
     fl_fwd = 2 * n * n * 128 * h  # causal: 4*n^2*d*h/2
     fl_bwd = 5 * n * n * 128 * h
     out = block_attn_update_final(q, k, v, None, MaskMode.Diagonal)
     t_fwd = timeit(lambda: block_attn_update_final(q, k, v, None, MaskMode.Diagonal))
-    print(f"fwd  H={h} N={n}: {t_fwd:.3f} ms  {fl_fwd / t_fwd / 1e9:.1f} TFLOP/s", flush=True)
+    print(f"fwd  H={h}/{hkv} N={n}: {t_fwd:.3f} ms  {fl_fwd / t_fwd / 1e9:.1f} TFLOP/s", flush=True)
     d_out = (torch.rand_like(out.o, dtype=torch.float32) * 2 - 1).to(torch.bfloat16)
     dvec = backward_aux(d_out, out.o)
     from paper_2310_03294_b200.flashcore import ChunkGrads
-    grads = ChunkGrads(torch.zeros(h, n, 128, device="cuda"), torch.empty(h, n, 128, device="cuda"),
-                       torch.empty(h, n, 128, device="cuda"))
+    grads = ChunkGrads(torch.zeros(h, n, 128, device="cuda"), torch.empty(hkv, n, 128, device="cuda"),
+                       torch.empty(hkv, n, 128, device="cuda"))
     def bwd():
         block_attn_backward(q, k, v, out.o, out.lse, d_out, MaskMode.Diagonal, d_vec=dvec, grads=grads)
     t_bwd = timeit(bwd)
