@@ -7,8 +7,9 @@ d=128), causal fwd+bwd at seq 32K on one B200, synthetic U[-1,1) bf16 inputs
 generated on the device. One step = one forward (block_attn_update with the
 fused finalize) + backward_aux + block_attn_backward over the full sequence.
 N>1 runs the sequence-parallel runtime (paper_2310_03294_b200/dist.py): the
-sequence is split into N contiguous chunks, one per rank, balanced forward
-schedule + ring backward, K/V over NCCL.
+sequence is split into N contiguous chunks, one per rank (32K tokens per GPU),
+balanced forward + balanced backward schedules, messages pulled by the copy
+engines from the peers' HBM (--transport peer, default) or NCCL send/recv.
 
 Metric: whole-job attention fwd+bwd TFLOP/s (algorithmic causal FLOPs
 7·N²·d·H per step, no recompute counted), with tokens/s and per-GPU TFLOP/s
@@ -306,6 +307,8 @@ def main(argv=None):
     ap.add_argument("--heads-per-group", type=int, default=1)
     ap.add_argument("--fwd-schedule", default="balanced", choices=["ring", "balanced", "balanced_split"])
     ap.add_argument("--bwd-schedule", default="balanced", choices=["ring", "balanced"])
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="N>1: copy-engine pulls from peer HBM (no SM use) or NCCL send/recv")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the torchrun/NCCL path even at one rank (tests the N>1 code)")

@@ -196,6 +196,19 @@ int64_t da_schedule_validate_backward(int workers, int32_t steps, const int32_t*
                                       int64_t n_messages);
 
 /* ------------------------------------------------------------------------
+ * Peer-memory transport signals (replaces the message channel of the
+ * reference's concurrent executor, runtime.cpp:413-487, for one process per
+ * GPU): 32-bit monotonic counters in device memory, written and awaited by
+ * stream memory operations, so ranks order their copy-engine pulls from each
+ * other's HBM without host synchronisation or NCCL kernels.
+ *   da_stream_write_u32:    *addr = value once prior work on `stream` is done
+ *   da_stream_wait_u32_geq: `stream` waits until (int)(*addr - value) >= 0
+ * addr may be local or a peer allocation mapped through CUDA IPC.
+ * ------------------------------------------------------------------------ */
+da_status da_stream_write_u32(void* stream, void* addr, uint32_t value);
+da_status da_stream_wait_u32_geq(void* stream, const void* addr, uint32_t value);
+
+/* ------------------------------------------------------------------------
  * Runtime (runtime.cpp:491-529, 720-750), P logical workers on ONE device —
  * the reference's stepper executor with device kernels: per step, every
  * worker's action runs in schedule order; "messages" are device buffers.

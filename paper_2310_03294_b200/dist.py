@@ -28,6 +28,7 @@ the test-suite; the production backend (CudaBackend) is the sm_100a library.
 """
 from __future__ import annotations
 
+import ctypes as C
 import math
 import os
 from dataclasses import dataclass
@@ -92,21 +93,29 @@ class CudaBackend:
 class Transport:
     """Point-to-point messages over torch.distributed (NCCL on GPU, gloo on CPU).
 
-    Ranks are 0-based; schedule workers are rank + 1."""
+    Ranks are 0-based; schedule workers are rank + 1. A receive is
+    (slot, src_rank, key): the key names the sender's published tensor and is
+    only used by the pull-based PeerTransport."""
 
     def __init__(self, group=None):
         self.group = group
         self.nccl = tdist.get_backend(group) == "nccl"
+        self.cuda = self.nccl
         self.stream = torch.cuda.Stream() if self.nccl else None
 
+    def publish(self, tensors: dict):
+        """No-op: NCCL/gloo move data by send/recv pairs."""
+
     def exchange(self, sends, recvs):
-        """Posts sends [(tensor, dst_rank)] and recvs [(tensor, src_rank)] as one
-        group. On NCCL the group starts only after everything already enqueued
-        on the current (compute) stream — so send data is produced and receive
-        slots are no longer read — and the returned handle's wait() orders the
-        current stream after the whole group. On gloo wait() blocks."""
+        """Posts sends [(tensor, dst_rank)] and recvs [(tensor, src_rank, key)] as
+        one group. On NCCL the group starts only after everything already
+        enqueued on the current (compute) stream — so send data is produced and
+        receive slots are no longer read — and the returned handle's wait()
+        orders the current stream after the whole group. On gloo wait() blocks."""
         if not sends and not recvs:
             return _Done()
+        sends = [(x[0], x[1]) for x in sends]
+        recvs = [(x[0], x[1]) for x in recvs]
         if self.nccl:
             ready = torch.cuda.Event()
             ready.record()
@@ -119,6 +128,122 @@ class Transport:
         works = [tdist.isend(t, r, self.group) for t, r in sends] + \
                 [tdist.irecv(t, r, self.group) for t, r in recvs]
         return _Works(works)
+
+
+class PeerTransport:
+    """Peer-memory transport: copy-engine pulls from the other ranks' HBM.
+
+    Every rank publishes the tensors it sends (CUDA IPC mappings, exchanged
+    once per buffer with a host all_gather_object and cached); a receive is a
+    cudaMemcpyAsync on a side stream straight from the sender's tensor into
+    the local slot — over NVLink between GPUs, with no NCCL kernels, so the
+    attention kernels keep every SM. Ordering is carried by 32-bit counters in
+    device memory (csrc/peer.cu): per destination a "ready" counter bumped on
+    the sender's compute stream when the data is produced, per source a
+    "done" counter bumped after the pull. The receiver's side stream waits on
+    the sender's ready counter, the sender's wait() on the receiver's done
+    counter — all in-stream, no host synchronisation on the data path.
+    Messages between a pair are matched by order, exactly as the schedule
+    emits them on both sides.
+    """
+
+    def __init__(self, group=None, device=None):
+        from torch.multiprocessing.reductions import reduce_tensor
+        from . import _lib
+        self._reduce = reduce_tensor
+        self.lib = _lib.lib()
+        self.group = group
+        self.nccl = False
+        self.cuda = True
+        self.rank = tdist.get_rank(group)
+        self.world = tdist.get_world_size(group)
+        self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.stream = torch.cuda.Stream(self.device)
+        w = self.world
+        # [0, w): ready counters, one per destination; [w, 2w): done counters, one per source
+        self.flags = torch.zeros(2 * w, dtype=torch.int32, device=self.device)
+        self.sent = [0] * w
+        self.pulled = [0] * w
+        self._mine = {}     # key -> (data_ptr, numel, dtype) last published
+        self.remote = {}    # (rank, key) -> tensor mapped from the peer
+        allf = self._gather({"__flags__": self._reduce(self.flags)})
+        self.remote_flags = [None] * w
+        for r, d in enumerate(allf):
+            self.remote_flags[r] = self.flags if r == self.rank else self._rebuild(d["__flags__"])
+
+    @staticmethod
+    def _rebuild(red):
+        fn, args = red
+        return fn(*args)
+
+    def _gather(self, obj):
+        out = [None] * self.world
+        tdist.all_gather_object(out, obj, group=self.group)
+        return out
+
+    def publish(self, tensors: dict):
+        """Collective: makes `tensors` pullable by every peer under their keys."""
+        mine = {}
+        for key, t in tensors.items():
+            sig = (t.data_ptr(), t.numel(), t.dtype)
+            if self._mine.get(key) != sig:
+                mine[key] = self._reduce(t)
+                self._mine[key] = sig
+        for r, d in enumerate(self._gather(mine)):
+            if r == self.rank:
+                continue
+            for key, red in d.items():
+                self.remote[(r, key)] = self._rebuild(red)
+
+    def _write(self, stream, idx, value):
+        from .errors import check
+        check(self.lib.da_stream_write_u32(C.c_void_p(stream.cuda_stream),
+                                           C.c_void_p(self.flags.data_ptr() + 4 * idx),
+                                           value & 0xFFFFFFFF))
+
+    def _wait(self, stream, rank, idx, value):
+        from .errors import check
+        check(self.lib.da_stream_wait_u32_geq(
+            C.c_void_p(stream.cuda_stream),
+            C.c_void_p(self.remote_flags[rank].data_ptr() + 4 * idx), value & 0xFFFFFFFF))
+
+    def exchange(self, sends, recvs):
+        if not sends and not recvs:
+            return _Done()
+        cur = torch.cuda.current_stream(self.device)
+        w, me = self.world, self.rank
+        expect = {}
+        for x in sends:
+            dst = x[1]
+            self.sent[dst] += 1
+            self._write(cur, dst, self.sent[dst])  # produced in stream order on `cur`
+            expect[dst] = self.sent[dst]
+        done = None
+        if recvs:
+            ready = torch.cuda.Event()
+            ready.record(cur)  # receive slots are no longer read by earlier work
+            self.stream.wait_event(ready)
+            with torch.cuda.stream(self.stream):
+                for slot, src, key in recvs:
+                    self.pulled[src] += 1
+                    self._wait(self.stream, src, me, self.pulled[src])
+                    slot.copy_(self.remote[(src, key)], non_blocking=True)
+                    self._write(self.stream, w + src, self.pulled[src])
+            done = torch.cuda.Event()
+            done.record(self.stream)
+        return _PeerWork(self, cur, done, expect)
+
+
+class _PeerWork:
+    def __init__(self, tr, stream, done, expect):
+        self.tr, self.stream, self.done, self.expect = tr, stream, done, expect
+
+    def wait(self):
+        cur = torch.cuda.current_stream(self.tr.device)
+        if self.done is not None:
+            cur.wait_event(self.done)
+        for dst, n in self.expect.items():  # the peers pulled what I sent
+            self.tr._wait(cur, dst, self.tr.world + self.tr.rank, n)
 
 
 class _Done:
@@ -393,7 +518,7 @@ class DistRuntime:
         h, rows, d = q.shape
         hk = k.shape[0]
         be, tr = self.backend, self.transport
-        rec = self.rec = Recorder(tr.nccl, tr.group, trace)
+        rec = self.rec = Recorder(tr.cuda, tr.group, trace)
         acc, _ = be.new_acc(h, rows, d, self._buf("acc", (h * rows * (d + 2),), be.acc_dtype))
         have_acc = False
         # receive slots: double-buffered (prefetch depth 1)
@@ -418,6 +543,11 @@ class DistRuntime:
             kvh_slot = (self._buf("kh_recv", (hk, rows - lo, d), k.dtype),
                         self._buf("vh_recv", (hk, rows - lo, d), v.dtype))
 
+        pub = {"k": k, "v": v, "q": q, "part": part_pk}
+        if any(p.part != 0 for p in plans) or any(p.kvh_sends for p in plans):
+            pub.update(k_hi=k_hi, v_hi=v_hi)
+        tr.publish(pub)  # collective (pull transport); no-op for send/recv transports
+
         def post_operands(t):
             """sends of my immutable KV/Q for step t + the receive my step-t action needs."""
             p = plans[t]
@@ -436,12 +566,12 @@ class DistRuntime:
                 self._sent(q)
                 rec.send(t, 1, w, dst, mk)
             if p.action == "direct" and p.part == KVPart.High:
-                recvs += [(kvh_slot[0], p.peer - 1), (kvh_slot[1], p.peer - 1)]
+                recvs += [(kvh_slot[0], p.peer - 1, "k_hi"), (kvh_slot[1], p.peer - 1, "v_hi")]
             elif p.action == "direct":
                 ks, vs = kv_slot[t % 2]
-                recvs += [(ks, p.peer - 1), (vs, p.peer - 1)]
+                recvs += [(ks, p.peer - 1, "k"), (vs, p.peer - 1, "v")]
             elif p.action == "help":
-                recvs.append((q_slot[t % 2], p.peer - 1))
+                recvs.append((q_slot[t % 2], p.peer - 1, "q"))
             return tr.exchange(sends, recvs)
 
         held = 0
@@ -488,7 +618,7 @@ class DistRuntime:
                 if buf is None:
                     buf = self._buf(f"part_recv{hw}", (h * rows * (d + 2),), be.acc_dtype)
                     recv_part[hw] = buf
-                tr.exchange([], [(buf, hw - 1)]).wait()
+                tr.exchange([], [(buf, hw - 1, "part")]).wait()
                 m0 = rec.mark()
                 rec.arrive(t, 2, hw, w, m0, [buf])
                 pa, _ = be.new_acc(h, rows, d, buf)
@@ -523,7 +653,7 @@ class DistRuntime:
         if viol:
             raise ScheduleError(f"invalid schedule: {viol[0]} ({len(viol)} violations)")
         plans = backward_plan(sched, w)
-        rec = self.rec_bwd = Recorder(tr.nccl, tr.group, trace)
+        rec = self.rec_bwd = Recorder(tr.cuda, tr.group, trace)
         gd = be.grad_dtype
         dq = self._buf("dq", (h, rows, d), gd)
         dk = self._buf("dk", (hk, rows, d), gd)
@@ -540,6 +670,9 @@ class DistRuntime:
                   for i in range(2)]
         q_send = [self._buf(f"gq{i}", (h, rows, d), gd) for i in range(2)]
         g_recv = (self._buf("grk", (hk, rows, d), gd), self._buf("grv", (hk, rows, d), gd))
+        tr.publish({"k": k, "v": v, "q": q, "d_out": d_out, "lse": lse, "d_vec": d_vec,
+                    "gk0": g_send[0][0], "gv0": g_send[0][1], "gk1": g_send[1][0],
+                    "gv1": g_send[1][1], "gq0": q_send[0], "gq1": q_send[1]})
 
         def post_operands(t):
             p = plans[t]
@@ -555,9 +688,10 @@ class DistRuntime:
                 rec.send(t, 1, w, dst, mk)
             if p.action == "direct":
                 ks, vs = kv_slot[t % 2]
-                recvs += [(ks, p.peer - 1), (vs, p.peer - 1)]
+                recvs += [(ks, p.peer - 1, "k"), (vs, p.peer - 1, "v")]
             elif p.action == "help":
-                recvs += [(x, p.peer - 1) for x in bundle[t % 2]]
+                recvs += [(x, p.peer - 1, key) for x, key in
+                          zip(bundle[t % 2], ("q", "d_out", "lse", "d_vec"))]
             return tr.exchange(sends, recvs)
 
         held = 0
@@ -594,13 +728,13 @@ class DistRuntime:
                 sends.append((gq, p.peer - 1))
                 self._sent(gq)
                 rec.send(t, 2, w, p.peer, m1)
-            recvs = [(g_recv[0], s - 1) for s in p.gradkv_from[:1]] + \
-                    [(g_recv[1], s - 1) for s in p.gradkv_from[:1]]
+            recvs = [(g_recv[0], s - 1, f"gk{t % 2}") for s in p.gradkv_from[:1]] + \
+                    [(g_recv[1], s - 1, f"gv{t % 2}") for s in p.gradkv_from[:1]]
             part_bufs = []
             for hw in p.merges:
                 buf = self._buf(f"gqr{hw}", (h, rows, d), gd)
                 part_bufs.append(buf)
-                recvs.append((buf, hw - 1))
+                recvs.append((buf, hw - 1, f"gq{t % 2}"))
             if len(p.gradkv_from) > 1:
                 raise ScheduleError("at most one GradKV per worker and step is supported")
             # results leave right after their kernels; waiting also retires the
@@ -633,8 +767,8 @@ class DistRuntime:
 # ----------------------------------------------------------------------------- bench (N > 1)
 def bench_main(args) -> int:
     """torchrun entry for bench.py --gpus N: sequence-parallel fwd+bwd of the
-    Llama-7B attention layer at seq 32K x N (32K tokens per GPU, weak scaling)
-    over NCCL. Device-timed steps (barrier + synchronize on both sides, max over
+    Llama-7B attention layer at seq 32K x N (32K tokens per GPU, weak scaling);
+    messages by copy-engine pulls over NVLink (PeerTransport, default) or NCCL. Device-timed steps (barrier + synchronize on both sides, max over
     ranks), then an e2e pass that copies each rank's q/k/v/dO shard in from
     pinned host memory and its bf16 dq/dk/dv out inside the timed region."""
     import json
@@ -652,7 +786,8 @@ def bench_main(args) -> int:
     n_total = rows * world
     torch.manual_seed(1234 + rank)
     q, k, v, do = [(torch.rand(heads, rows, d, device=dev) * 2 - 1).to(torch.bfloat16) for _ in range(4)]
-    rt = DistRuntime(rank, world, device=dev)
+    transport = PeerTransport(device=dev) if getattr(args, "transport", "peer") == "peer" else None
+    rt = DistRuntime(rank, world, device=dev, transport=transport)
     fwd_s = getattr(args, "fwd_schedule", "balanced")
     bwd_s = getattr(args, "bwd_schedule", "balanced")
 
@@ -733,7 +868,7 @@ def bench_main(args) -> int:
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
                 "config": {"workload": f"llama7b-attn causal fwd+bwd, {heads} heads, d=128, seq "
                                        f"{n_total} over {world} B200 ({fwd_s} fwd + {bwd_s} bwd, "
-                                       f"NCCL)",
+                                       f"{getattr(args, 'transport', 'peer')} transport)",
                            "heads": heads, "d": d, "seq_len": n_total, "tokens_per_gpu": rows,
                            "l2": "inputs exceed L2; no flush"},
                 "tokens_per_s": n_total / (ms * 1e-3),
