@@ -166,10 +166,12 @@ class PeerTransport:
         self.pulled = [0] * w
         self._mine = {}     # key -> (data_ptr, numel, dtype) last published
         self.remote = {}    # (rank, key) -> tensor mapped from the peer
-        allf = self._gather({"__flags__": self._reduce(self.flags)})
-        self.remote_flags = [None] * w
-        for r, d in enumerate(allf):
-            self.remote_flags[r] = self.flags if r == self.rank else self._rebuild(d["__flags__"])
+        self.remote_flags = [self.flags] * w
+        if w > 1:
+            allf = self._gather({"__flags__": self._reduce(self.flags)})
+            for r, d in enumerate(allf):
+                if r != self.rank:
+                    self.remote_flags[r] = self._rebuild(d["__flags__"])
 
     @staticmethod
     def _rebuild(red):
@@ -183,6 +185,8 @@ class PeerTransport:
 
     def publish(self, tensors: dict):
         """Collective: makes `tensors` pullable by every peer under their keys."""
+        if self.world == 1:
+            return
         mine = {}
         for key, t in tensors.items():
             sig = (t.data_ptr(), t.numel(), t.dtype)
