@@ -26,9 +26,11 @@
 // Bound (measured): besides the five 128^3 GEMMs per (kv tile, q tile), each
 // pair reduce-adds a 64 KB fp32 dQ partial into L2 via TMA; at 32K x 32 heads
 // that is 69 GB of L2 reductions per launch, and removing it (experiment
-// build) takes the kernel from 21.1 to 17.4 ms, half of it to 19.9 ms — the
-// L2 fp32 reduction throughput (~3.3 TB/s here) co-bounds the backward with
-// the tensor pipe.
+// build) takes the kernel from 21.1 to 17.4 ms, half of it to 19.9 ms. Plain
+// TMA stores of the same bytes cost about as much (20.9 ms), LSU red.global
+// from registers far more (29.5 ms): the cost is the partial's path through
+// shared memory (64 KB STS + 64 KB TMA read per pair) competing with the MMA
+// operand traffic (256 KB per pair), not the L2 reduction itself.
 #include <cuda.h>
 #include <cuda_bf16.h>
 
