@@ -161,3 +161,34 @@ def test_balanced_split_forward(cuda, P, n, heads, heads_kv):
     tb = run_backward(shards)
     torch.cuda.synchronize()
     _check_against_oracle(shards, P, n, "balanced_split", heads, tf, tb, heads_kv=heads_kv)
+
+
+def test_p1_backward_is_the_single_chunk_kernel(cuda):
+    """test_runtime.cpp:201-213: with one worker the runtime backward is one
+    block_attn_backward call (dk/dv bitwise; dq to fp32 reduction order)."""
+    from paper_2310_03294_b200.flashcore import MaskMode, block_attn_backward
+    from paper_2310_03294_b200.runtime import make_parity_shards, run_backward, run_forward
+    shards = make_parity_shards(9, 1, 1024, 2, 128)
+    run_forward(shards, "ring")
+    run_backward(shards)
+    s = shards[0]
+    g = block_attn_backward(s.q, s.k, s.v, s.out, s.lse, s.d_out, MaskMode.Diagonal)
+    torch.cuda.synchronize()
+    assert torch.equal(g.dk, s.dk) and torch.equal(g.dv, s.dv)
+    assert float((g.dq - s.dq).abs().max() / g.dq.abs().max()) < 1e-5
+
+
+def test_invalid_schedule_and_mismatched_shards_are_rejected(cuda):
+    """test_runtime.cpp:278-287"""
+    from paper_2310_03294_b200 import schedule as S
+    from paper_2310_03294_b200.errors import ScheduleError, ShapeError
+    from paper_2310_03294_b200.runtime import make_parity_shards, run_forward
+    shards = make_parity_shards(1, 4, 512, 1, 128)
+    bad = S.build_ring_schedule(4)
+    bad.steps[1][1] = S.Task(S.TaskKind.Idle, 2)
+    with pytest.raises(ScheduleError):
+        run_forward(shards, bad)
+    small = make_parity_shards(1, 4, 512, 1, 128)
+    small[2].q = small[2].q[:, :64].contiguous()
+    with pytest.raises(ShapeError):
+        run_forward(small, "ring")
