@@ -92,6 +92,29 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
     return LIB
 
 
+def build_cpp_tests() -> Path:
+    """tests/cpp/_build/test_b200_api: the C++ drop-in API (include/distattn/b200.hpp)
+    against the C oracle. Needs libdistattn_b200.so and oracle/liboracle.so."""
+    out_dir = ROOT / "tests" / "cpp" / "_build"
+    out_dir.mkdir(parents=True, exist_ok=True)
+    exe = out_dir / "test_b200_api"
+    src = ROOT / "tests" / "cpp" / "test_b200_api.cpp"
+    deps = [src, ROOT / "include" / "distattn" / "b200.hpp", ROOT / "include" / "distattn_b200.h", LIB]
+    if exe.exists() and exe.stat().st_mtime >= _newest(deps):
+        return exe
+    cuda = Path(nvcc()).resolve().parents[1]
+    cxx = shutil.which("g++") or "g++"
+    cmd = [cxx, "-std=c++17", "-O2", "-Wall", "-I", str(ROOT / "include"), "-I", str(ROOT / "oracle"),
+           "-I", str(cuda / "include"), str(src), "-o", str(exe),
+           "-L", str(PKG), "-ldistattn_b200", "-L", str(ROOT / "oracle"), "-loracle",
+           "-L", str(cuda / "lib64"), "-lcudart_static", "-ldl", "-lrt", "-lpthread",
+           "-Wl,-rpath,$ORIGIN/../../../paper_2310_03294_b200", "-Wl,-rpath,$ORIGIN/../../../oracle"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"C++ API test build failed:\n{r.stdout}\n{r.stderr}")
+    return exe
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose="-v" in sys.argv, ptxas_v="--ptxas" in sys.argv)
     print(LIB)
