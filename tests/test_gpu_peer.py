@@ -65,7 +65,8 @@ def _rel(a, b):
 @pytest.mark.parametrize("world,n,heads,fwd,bwd", [(2, 1024, 2, "balanced", "ring"),
                                                    (4, 2048, 1, "balanced", "balanced"),
                                                    (3, 768, 2, "ring", "balanced"),
-                                                   (4, 1024, 2, "balanced_split", "ring")])
+                                                   (4, 1024, 2, "balanced_split", "ring"),
+                                                   (2, 16384, 4, "balanced", "balanced")])
 def test_peer_runtime_one_process_per_rank(cuda, world, n, heads, fwd, bwd):
     with tempfile.TemporaryDirectory() as td:
         mp.spawn(_worker, args=(world, _port(), n, heads, fwd, bwd, td), nprocs=world, join=True)
