@@ -33,7 +33,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, n, heads, fwd, bwd, outdir):
+def _worker(rank, world, port, n, heads, fwd, bwd, outdir, heads_kv=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     tdist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -46,8 +46,9 @@ def _worker(rank, world, port, n, heads, fwd, bwd, outdir):
         t = lambda a: torch.from_numpy(np.ascontiguousarray(a[:, sl])).to(dev).to(torch.bfloat16)  # noqa: E731
         rt = DistRuntime(rank, world, backend=CudaBackend(dev), transport=PeerTransport(device=dev),
                          device=dev)
+        hk = heads_kv or heads
         for _ in range(2):  # the second pass reuses the published buffers and counters
-            out, lse = rt.forward(t(q), t(k), t(v), fwd)
+            out, lse = rt.forward(t(q), t(k[:hk]), t(v[:hk]), fwd)
             dq, dk, dv = rt.backward(t(do), bwd)
         torch.cuda.synchronize()
         np.savez(os.path.join(outdir, f"r{rank}.npz"), out=out.float().cpu().numpy(),
@@ -62,28 +63,37 @@ def _rel(a, b):
     return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
 
 
-@pytest.mark.parametrize("world,n,heads,fwd,bwd", [(2, 1024, 2, "balanced", "ring"),
-                                                   (4, 2048, 1, "balanced", "balanced"),
-                                                   (3, 768, 2, "ring", "balanced"),
-                                                   (4, 1024, 2, "balanced_split", "ring"),
-                                                   (2, 16384, 4, "balanced", "balanced")])
-def test_peer_runtime_one_process_per_rank(cuda, world, n, heads, fwd, bwd):
+@pytest.mark.parametrize("world,n,heads,fwd,bwd,heads_kv", [
+    (2, 1024, 2, "balanced", "ring", None), (4, 2048, 1, "balanced", "balanced", None),
+    (3, 768, 2, "ring", "balanced", None), (4, 1024, 2, "balanced_split", "ring", None),
+    (2, 8192, 2, "balanced", "balanced", None), (4, 1024, 4, "balanced", "balanced", 2)])
+def test_peer_runtime_one_process_per_rank(cuda, world, n, heads, fwd, bwd, heads_kv):
     with tempfile.TemporaryDirectory() as td:
-        mp.spawn(_worker, args=(world, _port(), n, heads, fwd, bwd, td), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _port(), n, heads, fwd, bwd, td, heads_kv), nprocs=world,
+                 join=True)
         res = [np.load(os.path.join(td, f"r{r}.npz")) for r in range(world)]
     got = {f: np.concatenate([r[f] for r in res], axis=1) for f in ("out", "lse", "dq", "dk", "dv")}
     q, k, v, do = O.make_inputs(0, world, n, 128, heads, bf16=True)
+    hk_n = heads_kv or heads
+    group = heads // hk_n
+    dk_ref = np.zeros((hk_n, n, 128))
+    dv_ref = np.zeros((hk_n, n, 128))
     for h in range(heads):
-        o_r, l_r, _ = O.run_forward(q[h], k[h], v[h], world, fwd)
+        j = h // group  # GQA parity: MHA with the group's K/V replicated
+        o_r, l_r, _ = O.run_forward(q[h], k[j], v[j], world, fwd)
         if bwd == "ring":
-            dq_r, dk_r, dv_r, _ = O.run_backward(q[h], k[h], v[h], o_r, l_r, do[h], world)
+            dq_r, dk_r, dv_r, _ = O.run_backward(q[h], k[j], v[j], o_r, l_r, do[h], world)
         else:
-            dq_r, dk_r, dv_r, _ = O.run_backward_sched(q[h], k[h], v[h], o_r, l_r, do[h], world, bwd)
+            dq_r, dk_r, dv_r, _ = O.run_backward_sched(q[h], k[j], v[j], o_r, l_r, do[h], world, bwd)
         assert _rel(got["out"][h], o_r) < TOL
         assert np.abs(got["lse"][h] - l_r).max() < LSE_TOL
         assert _rel(got["dq"][h], dq_r) < TOL
-        assert _rel(got["dk"][h], dk_r) < TOL
-        assert _rel(got["dv"][h], dv_r) < TOL
+        dk_ref[j] += dk_r
+        dv_ref[j] += dv_r
+    assert _rel(got["dk"], dk_ref) < TOL
+    assert _rel(got["dv"], dv_ref) < TOL
+    if heads_kv:
+        return
     # forward bitwise equal to the single-process device executor (same kernels, same order)
     from paper_2310_03294_b200.runtime import make_parity_shards, run_forward
     shards = make_parity_shards(0, world, n, heads, 128)
