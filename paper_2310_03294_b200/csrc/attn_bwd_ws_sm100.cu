@@ -40,6 +40,18 @@
 namespace da {
 namespace bwdws {
 
+#ifdef DA_TRACE
+#define BWS_TRACE(cond, it, slot)                                             \
+  do {                                                                        \
+    if ((cond) && p.trace != nullptr && blockIdx.x == 0 && (it) < 64)         \
+      p.trace[(it) * 16 + (slot)] = clock64();                                \
+  } while (0)
+#else
+#define BWS_TRACE(cond, it, slot) \
+  do {                            \
+  } while (0)
+#endif
+
 constexpr int kBM = 128;  // query rows per iteration
 constexpr int kBN = 128;  // kv rows per CTA
 constexpr int kHD = 128;
@@ -260,6 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool has_next = it + 1 < n_it;
         // dV += P^T dO
         mbar_wait(&bars->p_full, it & 1);
+        BWS_TRACE(true, it, 0);
         tc_fence_after();
         gemm_ts(tmem + kColDV, tmem + kColS, do_addr, it > 0);
         mma_commit(&bars->do_empty);
@@ -275,6 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // dK += dS^T Q, then dQ^T = K^T dS^T over the same region (in order)
         mbar_wait(&bars->ds_full, it & 1);
+        BWS_TRACE(true, it, 1);
         tc_fence_after();
         gemm_ts(tmem + kColDK, tmem + kColDP, q_addr + st * kTileBytes, it > 0);
         mma_commit(&bars->q_empty[st]);
@@ -288,6 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // next dP^T once dQ^T has left TMEM
         if (has_next) {
           mbar_wait(&bars->dq_drained, it & 1);
+          BWS_TRACE(true, it, 2);
           mbar_wait(&bars->do_full, (it + 1) & 1);
           tc_fence_after();
           gemm_kk(tmem + kColDP, v_addr, do_addr);
@@ -308,6 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int hq = cur.hq;
       const int row0 = cur.qt * kBM;
       mbar_wait(&bars->dq_full, it & 1);
+      BWS_TRACE(dw == 0 && lane == 0, it, 8);
       tc_fence_after();
       uint32_t r[4][32];
 #pragma unroll
@@ -315,6 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&bars->dq_drained);
+      BWS_TRACE(dw == 0 && lane == 0, it, 9);
       // deterministic order: the partials of query tile (hq, qt) are added by
       // descending kv tile; wait until every higher contributor has landed
       int* sem = nullptr;
@@ -370,6 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float* lse2 = vecs + st * 256;  // -lse * log2(e)
       mbar_wait(&bars->vec_full[st], (it >> 1) & 1);
       mbar_wait(&bars->s_full, it & 1);
+      BWS_TRACE(quarter == 0 && lane == 0, it, 3);
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < 4; ++c) {  // query columns [32 c, 32 c + 32)
@@ -402,6 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&bars->p_full);
+      BWS_TRACE(quarter == 0 && lane == 0, it, 4);
     }
     // ---- epilogue: dV rows
     if (n_it > 0) {
@@ -453,6 +472,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&bars->vec_full[st], (it >> 1) & 1);
       mbar_wait(&bars->p_full, it & 1);  // P(it) written (P warps)
       mbar_wait(&bars->dp_full, it & 1);
+      BWS_TRACE(quarter == 0 && lane == 0, it, 5);
       tc_fence_after();
       // P(it) (64 packed columns) into registers, then release the S region
       uint32_t pk[2][32];
@@ -461,6 +481,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&bars->p_read);
+      BWS_TRACE(quarter == 0 && lane == 0, it, 6);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {  // query columns [32 c, 32 c + 32)
         uint32_t dr[32];
@@ -499,6 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&bars->ds_full);
+      BWS_TRACE(quarter == 0 && lane == 0, it, 7);
     }
     // ---- epilogue: dK rows (scaled)
     if (n_it > 0) {
