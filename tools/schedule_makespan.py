@@ -22,6 +22,7 @@ from paper_2310_03294_b200 import flashcore as F  # noqa: E402
 from paper_2310_03294_b200 import schedule as S  # noqa: E402
 
 H, D = 32, 128
+HKV = H  # set by argv: python tools/schedule_makespan.py N [P ...] [--kv HKV]
 
 
 def timed(fn, iters=5):
@@ -39,14 +40,15 @@ def timed(fn, iters=5):
 def task_times(c):
     dev = "cuda"
     rnd = lambda *sh: (torch.rand(*sh, device=dev) * 2 - 1).to(torch.bfloat16)  # noqa: E731
-    q, k, v, do = rnd(H, c, D), rnd(H, c, D), rnd(H, c, D), rnd(H, c, D)
+    q, do = rnd(H, c, D), rnd(H, c, D)
+    k, v = rnd(HKV, c, D), rnd(HKV, c, D)
     kh, vh = k[:, : c // 2].contiguous(), v[:, : c // 2].contiguous()
     acc = F.block_attn_update(q, k, v, None, F.MaskMode.Diagonal)
     part = F.block_attn_update(q, k, v, None, F.MaskMode.Full)
     out = F.finalize(acc)
     dvec = F.backward_aux(do, out.o)
-    g = F.ChunkGrads(torch.zeros(H, c, D, device=dev), torch.zeros(H, c, D, device=dev),
-                     torch.zeros(H, c, D, device=dev))
+    g = F.ChunkGrads(torch.zeros(H, c, D, device=dev), torch.zeros(HKV, c, D, device=dev),
+                     torch.zeros(HKV, c, D, device=dev))
     t = {
         "fwd_diag": timed(lambda: F.block_attn_update(q, k, v, acc, F.MaskMode.Diagonal, out=acc)),
         "fwd_full": timed(lambda: F.block_attn_update(q, k, v, acc, F.MaskMode.Full, out=acc)),
@@ -83,9 +85,15 @@ def makespan(s, t, fwd=True):
 
 
 def main():
-    n = int(sys.argv[1]) if len(sys.argv) > 1 else 131072
-    ps = [int(x) for x in sys.argv[2:]] or [2, 4, 8]
-    res = {"seq": n, "heads": H, "d": D, "note": "compute critical path from measured chunk "
+    global HKV
+    args = sys.argv[1:]
+    if "--kv" in args:
+        i = args.index("--kv")
+        HKV = int(args[i + 1])
+        args = args[:i] + args[i + 2:]
+    n = int(args[0]) if args else 131072
+    ps = [int(x) for x in args[1:]] or [2, 4, 8]
+    res = {"seq": n, "heads": H, "heads_kv": HKV, "d": D, "note": "compute critical path from measured chunk "
            "kernels on one B200; communication assumed overlapped (projection, not a "
            "multi-GPU measurement)", "P": {}}
     for P in ps:
