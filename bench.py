@@ -307,8 +307,10 @@ def main(argv=None):
     ap.add_argument("--heads-per-group", type=int, default=1)
     ap.add_argument("--fwd-schedule", default="balanced", choices=["ring", "balanced", "balanced_split"])
     ap.add_argument("--bwd-schedule", default="balanced", choices=["ring", "balanced"])
+    ap.add_argument("--runtime", default="native", choices=["native", "python"],
+                    help="N>1: the C++ per-rank runtime (da_rank_*) or dist.DistRuntime")
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
-                    help="N>1: copy-engine pulls from peer HBM (no SM use) or NCCL send/recv")
+                    help="--runtime python: copy-engine pulls from peer HBM or NCCL send/recv")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the torchrun/NCCL path even at one rank (tests the N>1 code)")

@@ -493,6 +493,39 @@ inline CommCounters run_backward(std::vector<SequenceShard>& s, int64_t heads,
   return to_counters(c);
 }
 
+/// One rank of the sequence-parallel runtime, one process per GPU
+/// (runtime.cpp:390-487, 653-716 for a single worker): messages are
+/// copy-engine pulls from the peers' HBM. `allgather` bootstraps the IPC
+/// mappings (e.g. MPI_Allgather or torch.distributed); calls are collective.
+class RankRuntime {
+ public:
+  RankRuntime(int rank, int world, da_allgather_fn allgather, void* ctx) {
+    check(da_rank_create(rank, world, allgather, ctx, &h_));
+  }
+  ~RankRuntime() { da_rank_destroy(h_); }
+  RankRuntime(const RankRuntime&) = delete;
+  RankRuntime& operator=(const RankRuntime&) = delete;
+
+  /// run_forward for this rank's chunk; out / lse are kept as the backward's
+  /// saved state (the attention forward is never recomputed).
+  CommCounters forward(const Chunk& q, const Chunk& k, const Chunk& v, void* out, float* lse,
+                       da_schedule_kind kind, cudaStream_t st) {
+    da_counters c{};
+    check(da_rank_forward(h_, kind, q.data, k.data, v.data, q.heads, k.heads, q.rows, out, lse,
+                          &c, st));
+    return to_counters(c);
+  }
+  CommCounters backward(const void* d_out, float* dq, float* dk, float* dv, da_schedule_kind kind,
+                        cudaStream_t st) {
+    da_counters c{};
+    check(da_rank_backward(h_, kind, d_out, dq, dk, dv, &c, st));
+    return to_counters(c);
+  }
+
+ private:
+  da_rank* h_ = nullptr;
+};
+
 }  // namespace b200
 }  // namespace distattn
 

@@ -249,6 +249,35 @@ da_status da_run_backward_sched(const da_shards* shards, int schedule_kind, da_c
 /* Frees the cached runtime workspace of the calling thread. */
 void da_runtime_release(void);
 
+/* ------------------------------------------------------------------------
+ * Per-rank runtime: one process (or thread) per GPU, each holding ONE
+ * contiguous chunk of the sequence — the reference's worker (runtime.cpp:
+ * 390-487 concurrent executor, 653-716 backward) with every message a
+ * copy-engine pull from the peer's HBM (CUDA IPC, over NVLink between GPUs)
+ * ordered by device-side counters (da_stream_write_u32 / wait). No NCCL.
+ *
+ * Bootstrap and per-pass publication of the pulled buffers go through the
+ * caller's allgather (e.g. torch.distributed, MPI): `fn(ctx, send, bytes,
+ * recv)` must gather `bytes` from every rank into recv[world * bytes] in rank
+ * order and return 0. All da_rank_* calls are collective over the ranks.
+ * Forward: q [h_q, rows, 128], k/v [h_kv, rows, 128] bf16 of this rank;
+ * writes out (bf16) and lse (fp32) and keeps them (the rematerialisation
+ * state) for da_rank_backward, which writes fp32 dq [h_q], dk/dv [h_kv].
+ * schedule_kind: DA_SCHEDULE_RING / BALANCED / BALANCED_SPLIT (forward),
+ * DA_SCHEDULE_RING_BWD / BALANCED_BWD (backward).
+ * ------------------------------------------------------------------------ */
+typedef int (*da_allgather_fn)(void* ctx, const void* send, uint64_t bytes, void* recv);
+typedef struct da_rank da_rank;
+
+da_status da_rank_create(int rank, int world, da_allgather_fn fn, void* ctx, da_rank** out);
+void da_rank_destroy(da_rank* r);
+da_status da_rank_forward(da_rank* r, int schedule_kind, const void* q, const void* k,
+                          const void* v, int64_t h_q, int64_t h_kv, int64_t rows, void* out,
+                          float* lse, da_counters* counters, void* stream);
+da_status da_rank_backward(da_rank* r, int schedule_kind, const void* d_out, float* dq, float* dk,
+                           float* dv, da_counters* counters, void* stream);
+
+
 /* Device fill with the reference's splitmix64 stream (numerics.hpp:140-174):
  * out[i] = lo + (hi - lo) * unit(draw i of the stream whose CURRENT state is
  * `state`), stored as dtype 0 = fp32, 1 = bf16 (via fp32, round-to-nearest-

@@ -54,6 +54,10 @@ SIGNATURES = {
     "da_last_error": (C.c_char_p, []),
     "da_abi_version": (C.c_int, []),
     "da_stream_write_u32": (C.c_int, [vp, vp, C.c_uint32]),
+    "da_rank_create": (C.c_int, [C.c_int, C.c_int, vp, vp, C.POINTER(vp)]),
+    "da_rank_destroy": (None, [vp]),
+    "da_rank_forward": (C.c_int, [vp, C.c_int, vp, vp, vp, i64, i64, i64, vp, vp, vp, vp]),
+    "da_rank_backward": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, vp, vp]),
     "da_stream_wait_u32_geq": (C.c_int, [vp, vp, C.c_uint32]),
     "da_device_supported": (C.c_int, []),
     "da_attn_fwd_chunk": (C.c_int, [C.POINTER(FwdArgs), vp]),

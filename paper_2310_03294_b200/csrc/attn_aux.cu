@@ -158,6 +158,31 @@ cudaError_t launch_bwd_preprocess(const void* d_out, const void* out, float* d_v
   return cudaGetLastError();
 }
 
+__global__ void add_kernel(float4* __restrict__ dst, const float4* __restrict__ src, int64_t n4) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+       i += stride) {
+    float4 a = dst[i];
+    const float4 b = src[i];
+    a.x += b.x;
+    a.y += b.y;
+    a.z += b.z;
+    a.w += b.w;
+    dst[i] = a;
+  }
+}
+
+// dst += src (fp32, n a multiple of 4): GradKV / dq-partial folds of the per-rank runtime
+cudaError_t launch_add(float* dst, const float* src, int64_t n, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t n4 = n / 4;
+  const int64_t blocks = (n4 + 255) / 256;
+  const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
+  add_kernel<<<static_cast<unsigned>(blocks < cap ? blocks : cap), 256, 0, stream>>>(
+      reinterpret_cast<float4*>(dst), reinterpret_cast<const float4*>(src), n4);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_convert(const float* src, void* dst, int64_t n, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
   const int64_t n4 = n / 4;

@@ -61,6 +61,8 @@ cudaError_t launch_bwd_preprocess(const void* d_out, const void* out, float* d_v
 
 cudaError_t launch_convert(const float* src, void* dst, int64_t n, cudaStream_t stream);
 
+cudaError_t launch_add(float* dst, const float* src, int64_t n, cudaStream_t stream);
+
 cudaError_t launch_copy_acc(const float* o, const float* m, const float* l, float* o_out,
                             float* m_out, float* l_out, int64_t rows_total, cudaStream_t stream);
 

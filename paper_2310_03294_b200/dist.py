@@ -790,14 +790,24 @@ def bench_main(args) -> int:
     n_total = rows * world
     torch.manual_seed(1234 + rank)
     q, k, v, do = [(torch.rand(heads, rows, d, device=dev) * 2 - 1).to(torch.bfloat16) for _ in range(4)]
-    transport = PeerTransport(device=dev) if getattr(args, "transport", "peer") == "peer" else None
-    rt = DistRuntime(rank, world, device=dev, transport=transport)
     fwd_s = getattr(args, "fwd_schedule", "balanced")
     bwd_s = getattr(args, "bwd_schedule", "balanced")
+    native = getattr(args, "runtime", "native") == "native"
+    if native:
+        # the C++ per-rank runtime (csrc/rank_runtime.cu): copy-engine pulls
+        from .rank import RankRuntime
+        rt = RankRuntime(rank, world)
 
-    def step():
-        rt.forward(q, k, v, fwd_s)
-        return rt.backward(do, bwd_s)
+        def step():
+            rt.forward(q, k, v, fwd_s)
+            return rt.backward(do, bwd_s)[:3]
+    else:
+        transport = PeerTransport(device=dev) if getattr(args, "transport", "peer") == "peer" else None
+        rt = DistRuntime(rank, world, device=dev, transport=transport)
+
+        def step():
+            rt.forward(q, k, v, fwd_s)
+            return rt.backward(do, bwd_s)
 
     root = Path(__file__).resolve().parents[1]
     if str(root) not in _sys.path:
@@ -828,7 +838,7 @@ def bench_main(args) -> int:
         for dst, src in zip(dev_in, host_in):
             dst.copy_(src, non_blocking=True)
         rt.forward(dev_in[0], dev_in[1], dev_in[2], fwd_s)
-        grads = rt.backward(dev_in[3], bwd_s)
+        grads = rt.backward(dev_in[3], bwd_s)[:3]
         for src, dst in zip(grads, host_out):
             dst.copy_(src.to(torch.bfloat16), non_blocking=True)
 
@@ -872,7 +882,9 @@ def bench_main(args) -> int:
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
                 "config": {"workload": f"llama7b-attn causal fwd+bwd, {heads} heads, d=128, seq "
                                        f"{n_total} over {world} B200 ({fwd_s} fwd + {bwd_s} bwd, "
-                                       f"{getattr(args, 'transport', 'peer')} transport)",
+                                       + ("native C++ runtime, peer pulls)" if native else
+                                          f"python runtime, {getattr(args, 'transport', 'peer')} "
+                                          "transport)"),
                            "heads": heads, "d": d, "seq_len": n_total, "tokens_per_gpu": rows,
                            "l2": "inputs exceed L2; no flush"},
                 "tokens_per_s": n_total / (ms * 1e-3),
@@ -884,8 +896,9 @@ def bench_main(args) -> int:
                         "h2d_bytes_per_step": 4 * heads * n_total * d * 2,
                         "d2h_bytes_per_step": 3 * heads * n_total * d * 2,
                         "ms_per_step": ms_e2e,
-                        "path": "dist.DistRuntime forward/backward with pinned-host shards in "
-                                "and bf16 grads out, every rank"},
+                        "path": ("rank.RankRuntime (C++ da_rank_*)" if native else "dist.DistRuntime") +
+                                " forward/backward with pinned-host shards in and bf16 grads out, "
+                                "every rank"},
                 "gpu_launches": launches * args.steps,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)

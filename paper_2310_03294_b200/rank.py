@@ -1,0 +1,90 @@
+"""Python handle on the native per-rank runtime (csrc/rank_runtime.cu).
+
+The C++ runtime executes this rank's schedule (forward and backward) with
+copy-engine pulls from the peers' HBM; Python only supplies the bootstrap
+allgather (torch.distributed, any backend) and device tensors. Mirrors
+runtime.hpp's worker for one process per GPU (runtime.cpp:390-487, 653-716).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+import torch.distributed as tdist
+
+from . import _lib
+from .errors import check
+from .runtime import CommCounters
+
+_AG = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p)
+_FWD = {"ring": 0, "balanced": 1, "balanced_split": 4}
+_BWD = {"ring": 2, "balanced": 3}
+
+
+class RankRuntime:
+    """One rank of the sequence-parallel runtime; all calls are collective."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        self.rank, self.world, self.group = rank, world, group
+        self._cb = _AG(self._allgather)  # keep the trampoline alive
+        h = C.c_void_p()
+        check(_lib.lib().da_rank_create(rank, world, C.cast(self._cb, C.c_void_p), None,
+                                        C.byref(h)))
+        self._h = h
+        self._saved = None
+
+    def _allgather(self, ctx, send, nbytes, recv):
+        try:
+            mine = C.string_at(send, nbytes)
+            outs = [None] * self.world
+            tdist.all_gather_object(outs, mine, group=self.group)
+            C.memmove(recv, b"".join(outs), nbytes * self.world)
+            return 0
+        except Exception:  # pragma: no cover - surfaced as a ConfigError by the C side
+            return 1
+
+    def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                schedule: str = "balanced", stream=None):
+        h, rows, _ = q.shape
+        hk = k.shape[0]
+        out = torch.empty_like(q)
+        lse = torch.empty(h, rows, dtype=torch.float32, device=q.device)
+        c = _lib.Counters()
+        st = stream if stream is not None else torch.cuda.current_stream()
+        check(_lib.lib().da_rank_forward(self._h, _FWD[schedule], q.data_ptr(), k.data_ptr(),
+                                         v.data_ptr(), h, hk, rows, out.data_ptr(),
+                                         lse.data_ptr(), C.byref(c), st.cuda_stream))
+        self._saved = (q, k, v, out, lse)  # the runtime holds pointers to these
+        return out, lse, _counters(c)
+
+    def backward(self, d_out: torch.Tensor, schedule: str = "ring", stream=None):
+        q, k, v, out, lse = self._saved if self._saved else (None,) * 5
+        if q is None:
+            from .errors import StateError
+            raise StateError("run_backward requires forward output and logsumexp")
+        dq = torch.empty(q.shape, dtype=torch.float32, device=q.device)
+        dk = torch.empty(k.shape, dtype=torch.float32, device=q.device)
+        dv = torch.empty(k.shape, dtype=torch.float32, device=q.device)
+        c = _lib.Counters()
+        st = stream if stream is not None else torch.cuda.current_stream()
+        check(_lib.lib().da_rank_backward(self._h, _BWD[schedule], d_out.data_ptr(), dq.data_ptr(),
+                                          dk.data_ptr(), dv.data_ptr(), C.byref(c),
+                                          st.cuda_stream))
+        self._keep_dout = d_out
+        return dq, dk, dv, _counters(c)
+
+    def close(self):
+        if self._h:
+            _lib.lib().da_rank_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _counters(c) -> CommCounters:
+    return CommCounters(c.kv_scalars, c.q_scalars, c.partial_scalars, c.grad_scalars,
+                        c.kv_messages, c.q_messages, c.partial_messages, c.grad_messages)
