@@ -26,7 +26,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, n, heads, fwd, bwd, outdir):
+def _worker(rank, world, port, n, heads, fwd, bwd, outdir, heads_kv=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     tdist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -37,7 +37,8 @@ def _worker(rank, world, port, n, heads, fwd, bwd, outdir):
         sl = slice(rank * rows, (rank + 1) * rows)
         t = lambda a: torch.from_numpy(np.ascontiguousarray(a[:, sl])).cuda().to(torch.bfloat16)  # noqa: E731
         rt = RankRuntime(rank, world)
-        qq, kk, vv, dd = t(q), t(k), t(v), t(do)
+        hk = heads_kv or heads
+        qq, kk, vv, dd = t(q), t(k[:hk]), t(v[:hk]), t(do)
         for _ in range(2):  # second pass: cached mappings, running counters
             out, lse, cf = rt.forward(qq, kk, vv, fwd)
             dq, dk, dv, cb = rt.backward(dd, bwd)
@@ -57,28 +58,40 @@ def _rel(a, b):
     return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
 
 
-@pytest.mark.parametrize("world,n,heads,fwd,bwd", [(2, 1024, 2, "balanced", "ring"),
-                                                   (4, 2048, 1, "balanced", "balanced"),
-                                                   (3, 768, 2, "ring", "balanced"),
-                                                   (4, 1024, 2, "balanced_split", "ring")])
-def test_native_rank_runtime(cuda, world, n, heads, fwd, bwd):
+@pytest.mark.parametrize("world,n,heads,fwd,bwd,heads_kv", [
+    (2, 1024, 2, "balanced", "ring", None), (4, 2048, 1, "balanced", "balanced", None),
+    (3, 768, 2, "ring", "balanced", None), (4, 1024, 2, "balanced_split", "ring", None),
+    (1, 512, 2, "balanced", "ring", None), (2, 1002, 1, "balanced_split", "balanced", None),
+    (4, 1024, 4, "balanced", "balanced", 2)])
+def test_native_rank_runtime(cuda, world, n, heads, fwd, bwd, heads_kv):
+    """Worlds 1-4, ring / balanced / split forward, ring / balanced backward,
+    odd chunk rows (split halves 250 / 251), GQA (4 q / 2 kv heads)."""
     with tempfile.TemporaryDirectory() as td:
-        mp.spawn(_worker, args=(world, _port(), n, heads, fwd, bwd, td), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _port(), n, heads, fwd, bwd, td, heads_kv), nprocs=world,
+                 join=True)
         res = [np.load(os.path.join(td, f"r{r}.npz")) for r in range(world)]
     got = {f: np.concatenate([r[f] for r in res], axis=1) for f in ("out", "lse", "dq", "dk", "dv")}
     q, k, v, do = O.make_inputs(0, world, n, 128, heads, bf16=True)
+    hk = heads_kv or heads
+    group = heads // hk
+    dk_ref = np.zeros((hk, n, 128))
+    dv_ref = np.zeros((hk, n, 128))
     for h in range(heads):
-        o_r, l_r, c_f = O.run_forward(q[h], k[h], v[h], world, fwd)
+        j = h // group  # GQA parity: MHA with the group's K/V replicated
+        o_r, l_r, c_f = O.run_forward(q[h], k[j], v[j], world, fwd)
         if bwd == "ring":
-            dq_r, dk_r, dv_r, c_b = O.run_backward(q[h], k[h], v[h], o_r, l_r, do[h], world)
+            dq_r, dk_r, dv_r, c_b = O.run_backward(q[h], k[j], v[j], o_r, l_r, do[h], world)
         else:
-            dq_r, dk_r, dv_r, c_b = O.run_backward_sched(q[h], k[h], v[h], o_r, l_r, do[h], world,
+            dq_r, dk_r, dv_r, c_b = O.run_backward_sched(q[h], k[j], v[j], o_r, l_r, do[h], world,
                                                          bwd)
         assert _rel(got["out"][h], o_r) < TOL
         assert np.abs(got["lse"][h] - l_r).max() < LSE_TOL
         assert _rel(got["dq"][h], dq_r) < TOL
-        assert _rel(got["dk"][h], dk_r) < TOL
-        assert _rel(got["dv"][h], dv_r) < TOL
+        dk_ref[j] += dk_r
+        dv_ref[j] += dv_r
+    assert _rel(got["dk"], dk_ref) < TOL and _rel(got["dv"], dv_ref) < TOL
+    if heads_kv:
+        return
     # per-rank counters summed = the reference's CommCounters (x heads for scalars)
     cf = sum(r["cf"] for r in res)
     cb = sum(r["cb"] for r in res)
