@@ -7,12 +7,16 @@
 //   4 SS, N=256, one accumulator (counted as two 128^3 GEMMs)
 //   5 SS, four accumulators interleaved
 //   6 SS, N=64 x 2 interleaved (half-width tiles)
+//   7 SS, two accumulators issued one whole chain after the other
+//   8 SS, two accumulators interleaved two steps at a time
+//   9 TS chain then SS chain (independent accumulators, issued sequentially)
 // Reports the best of 3 runs, clk per 128^3 GEMM (ideal 512 at 4096 MAC/clk).
 #include <cstdio>
 #include <cstdint>
 #include "../../paper_2310_03294_b200/csrc/sm100_ptx.cuh"
 using namespace da;
 
+constexpr int kModes = 10;
 __global__ void __launch_bounds__(128, 1) kern(long long* out, int reps) {
   extern __shared__ __align__(1024) uint8_t raw[];
   uint8_t* smem = raw + smem_align_pad(raw);
@@ -45,7 +49,7 @@ __global__ void __launch_bounds__(128, 1) kern(long long* out, int reps) {
     const uint32_t kBox = 32768;  // room for 256-row boxes
     int phase = 0;
     for (int round = 0; round < 3; ++round)
-      for (int mode = 0; mode < 7; ++mode) {
+      for (int mode = 0; mode < kModes; ++mode) {
         const uint32_t nn = mode == 4 ? 256 : (mode == 6 ? 64 : 128);
         const uint32_t idesc = make_idesc_bf16(128, nn, false, false);
         long long t0 = clock64();
@@ -69,6 +73,18 @@ __global__ void __launch_bounds__(128, 1) kern(long long* out, int reps) {
             } else if (mode == 6) {
               mma_ss(tmem, da, db, idesc, acc);
               mma_ss(tmem + 64, da, db, idesc, acc);
+            } else if (mode == 7 || mode == 9) {
+              // handled below (sequential chains)
+            } else if (mode == 8) {
+              if ((kk & 1) == 0) {
+                const uint32_t off1 = ((kk + 1) >> 2) * kBox + ((kk + 1) & 3) * 32;
+                const uint64_t da1 = make_sdesc_sw128(a + off1, 16, 1024);
+                const uint64_t db1 = make_sdesc_sw128(b + off1, 16, 1024);
+                mma_ss(tmem, da, db, idesc, acc);
+                mma_ss(tmem, da1, db1, idesc, 1u);
+                mma_ss(tmem + 128, da, db, idesc, acc);
+                mma_ss(tmem + 128, da1, db1, idesc, 1u);
+              }
             } else if (mode == 2) {
               mma_ts(tmem, tmem + 384 + kk * 8, db, idesc, acc);
             } else {
@@ -76,13 +92,26 @@ __global__ void __launch_bounds__(128, 1) kern(long long* out, int reps) {
               mma_ts(tmem + 128, tmem + 384 + kk * 8, db, idesc, acc);
             }
           }
+          if (mode == 7 || mode == 9) {
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk) {
+                const uint32_t off = (kk >> 2) * kBox + (kk & 3) * 32;
+                const uint64_t da = make_sdesc_sw128(a + off, 16, 1024);
+                const uint64_t db = make_sdesc_sw128(b + off, 16, 1024);
+                const uint32_t acc = kk > 0 ? 1u : 0u;
+                if (mode == 9 && c == 0) mma_ts(tmem, tmem + 384 + kk * 8, db, idesc, acc);
+                else mma_ss(tmem + 128 * c, da, db, idesc, acc);
+              }
+          }
         }
         mma_commit(&bar);
         mbar_wait(&bar, phase & 1);
         ++phase;
         const long long dt = clock64() - t0;
         const double gemms = mode == 5 ? 4.0 * reps
-                             : (mode == 1 || mode == 3 || mode == 4) ? 2.0 * reps : 1.0 * reps;
+                             : (mode == 1 || mode == 3 || mode == 4 || mode >= 7) ? 2.0 * reps : 1.0 * reps;
         const long long per = static_cast<long long>(dt / gemms);
         if (round == 0 || per < out[mode]) out[mode] = per;
       }
@@ -92,15 +121,16 @@ __global__ void __launch_bounds__(128, 1) kern(long long* out, int reps) {
 }
 
 int main() {
-  long long* d; cudaMalloc(&d, 128);
+  long long* d; cudaMalloc(&d, 256);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
-  const char* names[7] = {"SS 1 accumulator", "SS 2 interleaved", "TS 1 accumulator",
-                          "TS 2 interleaved", "SS N=256", "SS 4 interleaved", "SS N=64 x2"};
+  const char* names[kModes] = {"SS 1 accumulator", "SS 2 interleaved", "TS 1 accumulator",
+                               "TS 2 interleaved", "SS N=256", "SS 4 interleaved", "SS N=64 x2",
+                               "SS 2 sequential", "SS 2 by pairs", "TS then SS"};
   for (int grid : {1, 148}) {
     kern<<<grid, 128, 200000>>>(d, 4000);
     cudaError_t e = cudaDeviceSynchronize();
-    long long h[7]; cudaMemcpy(h, d, 56, cudaMemcpyDeviceToHost);
-    for (int m = 0; m < 7; ++m)
+    long long h[kModes]; cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    for (int m = 0; m < kModes; ++m)
       printf("grid %3d  %-18s %lld clk per 128^3 GEMM (%s)\n", grid, names[m], h[m],
              cudaGetErrorString(e));
   }
