@@ -112,6 +112,62 @@ def test_bwd_chunk(cuda, h, hkv, n, diag):
     assert rel_err(grads.dq, dq) < TOL, "dq"
 
 
+@pytest.mark.parametrize("h,hkv,n,nk", [(2, 2, 300, 130), (4, 1, 128, 384), (2, 1, 1000, 260)])
+def test_bwd_full_ragged(cuda, h, hkv, n, nk):
+    """Full-mask chunk pair with rows_q != rows_kv and partial tiles on both sides
+    (the helper/direct tasks of uneven shards), GQA groups summed into dK/dV."""
+    from paper_2310_03294_b200.flashcore import MaskMode, block_attn_backward
+    q, k, v = _qkv(h, n, hkv, nk, seed=n + nk)
+    d_out = _qkv(h, n, seed=n * 3)[0]
+    o_ref, lse_ref = attention_ref(q, k, v, False)
+    grads = block_attn_backward(q, k, v, o_ref.to(torch.bfloat16), lse_ref.contiguous(), d_out,
+                                MaskMode.Full)
+    torch.cuda.synchronize()
+    dq, dk, dv = attention_grads_ref(q, k, v, d_out, False)
+    assert rel_err(grads.dv, dv) < TOL, "dv"
+    assert rel_err(grads.dk, dk) < TOL, "dk"
+    assert rel_err(grads.dq, dq) < TOL, "dq"
+
+
+@pytest.mark.parametrize("amp", [8.0, 24.0])
+def test_peaky_fwd_bwd_chunk_chain(cuda, amp):
+    """SURVEY §8(d) "peaky" set: q scaled so single keys dominate rows and the
+    running max moves between chunks; the chain diag(kv2) -> full(kv0) ->
+    full(kv1) + finalize and the backward over all three pairs match fp32."""
+    from paper_2310_03294_b200.flashcore import (MaskMode, block_attn_backward, block_attn_update,
+                                                 block_attn_update_final)
+    h, c = 2, 256
+    q, k, v = _qkv(h, 3 * c, seed=int(amp), amp=amp)
+    d_out = _qkv(h, 3 * c, seed=99)[0]
+    sl = [slice(i * c, (i + 1) * c) for i in range(3)]
+    qs, ks, vs = ([x[:, s_].contiguous() for s_ in sl] for x in (q, k, v))
+    acc = block_attn_update(qs[2], ks[2], vs[2], None, MaskMode.Diagonal)
+    acc = block_attn_update(qs[2], ks[0], vs[0], acc, MaskMode.Full, out=acc)
+    out = block_attn_update_final(qs[2], ks[1], vs[1], acc, MaskMode.Full)
+    o_ref, lse_ref = attention_ref(q, k, v, True)
+    assert rel_err(out.o, o_ref[:, sl[2]]) < TOL
+    assert (out.lse - lse_ref[:, sl[2]]).abs().max().item() < LSE_TOL
+    # backward of the last query chunk: dq summed over its three kv chunks
+    do2 = d_out[:, sl[2]].contiguous()
+    lse2 = lse_ref[:, sl[2]].contiguous()
+    o2 = o_ref[:, sl[2]].to(torch.bfloat16)
+    g = block_attn_backward(qs[2], ks[2], vs[2], o2, lse2, do2, MaskMode.Diagonal)
+    dks, dvs = [g.dk], [g.dv]
+    for j in (0, 1):
+        gj = block_attn_backward(qs[2], ks[j], vs[j], o2, lse2, do2, MaskMode.Full)
+        g.dq += gj.dq
+        dks.append(gj.dk)
+        dvs.append(gj.dv)
+    torch.cuda.synchronize()
+    d_full = torch.zeros_like(d_out)
+    d_full[:, sl[2]] = do2
+    dq, dk, dv = attention_grads_ref(q, k, v, d_full, True)
+    assert rel_err(g.dq, dq[:, sl[2]]) < TOL, "dq"
+    assert rel_err(dks[0], dk[:, sl[2]]) < TOL and rel_err(dvs[0], dv[:, sl[2]]) < TOL
+    assert rel_err(dks[1], dk[:, sl[0]]) < TOL and rel_err(dvs[1], dv[:, sl[0]]) < TOL
+    assert rel_err(dks[2], dk[:, sl[1]]) < TOL and rel_err(dvs[2], dv[:, sl[1]]) < TOL
+
+
 def test_single_gpu_fwd_bwd_32k_sampled(cuda):
     """cfg2 shape at 2 heads: full causal 32K forward+backward, rows sampled against fp32."""
     from paper_2310_03294_b200.flashcore import MaskMode, block_attn_backward, block_attn_update_final
