@@ -46,12 +46,36 @@ namespace bwdws {
     if ((cond) && p.trace != nullptr && blockIdx.x == 0 && (it) < 64)         \
       p.trace[(it) * 16 + (slot)] = clock64();                                \
   } while (0)
+// per-CTA record after the 64x16 iteration stamps: globaltimer start/end,
+// clock64 start/end, smid, iterations, first MMA issue, last MMA commit
+#define BWS_CTA_TRACE(slot, val)                                              \
+  do {                                                                        \
+    if (p.trace != nullptr)                                                   \
+      p.trace[1024 + static_cast<size_t>(blockIdx.x) * 8 + (slot)] = (val);   \
+  } while (0)
+__device__ __forceinline__ unsigned long long bws_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned long long bws_smid() {
+  uint32_t s;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+  return s;
+}
 #else
 #define BWS_TRACE(cond, it, slot) \
   do {                            \
   } while (0)
+#define BWS_CTA_TRACE(slot, val) \
+  do {                           \
+  } while (0)
 #endif
 
+#ifndef DA_BWD_HEAD_GROUP
+#define DA_BWD_HEAD_GROUP 1
+#endif
+constexpr int kHeadGroup = DA_BWD_HEAD_GROUP;
 constexpr int kBM = 128;  // query rows per iteration
 constexpr int kBN = 128;  // kv rows per CTA
 constexpr int kHD = 128;
@@ -96,6 +120,32 @@ struct Bars {
 };
 static_assert(sizeof(Bars) <= 1024, "barrier block");
 
+// dK/dV epilogue: each thread stores its accumulator row (TMEM lane) from
+// registers. (Staging the rows in the free smem tiles and writing them with TMA
+// stores measured ~5% slower overall: the bulk stores delay the next CTA's
+// loads on the same SM.)
+__device__ __forceinline__ void store_acc_rows_lsu(float* dst, bool valid, uint32_t tmem_cols,
+                                                   float f, bool accumulate) {
+#pragma unroll 1
+  for (int c = 0; c < 4; ++c) {
+    uint32_t a[32];
+    tmem_ld_32x32b_x32(tmem_cols + c * 32, a);
+    tmem_ld_wait();
+    if (!valid) continue;
+    float4* d4 = reinterpret_cast<float4*>(dst + c * 32);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float4 x = make_float4(f * __uint_as_float(a[4 * i]), f * __uint_as_float(a[4 * i + 1]),
+                             f * __uint_as_float(a[4 * i + 2]), f * __uint_as_float(a[4 * i + 3]));
+      if (accumulate) {
+        const float4 o = d4[i];
+        x.x += o.x; x.y += o.y; x.z += o.z; x.w += o.w;
+      }
+      d4[i] = x;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_ws_kernel(const __grid_constant__ CUtensorMap tmap_q,
                        const __grid_constant__ CUtensorMap tmap_k,
@@ -114,15 +164,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   // ---- work: head-major, within a head the kv tiles with most query tiles first
   const int n_q_tiles = (p.rows_q + kBM - 1) / kBM;
   const int n_kv_tiles = (p.rows_kv + kBN - 1) / kBN;
-  const int kv_head = static_cast<int>(blockIdx.x / n_kv_tiles);
+  // kv heads in groups of kHeadGroup, interleaved within a group (L2 holds the
+  // group's Q/dO; the last wave mixes heads instead of one head's tiles)
+  const int b = static_cast<int>(blockIdx.x);
+  const int g0 = (b / (kHeadGroup * n_kv_tiles)) * kHeadGroup;
+  const int g_heads = min(kHeadGroup, p.h_kv - g0);
+  const int r_in = b - g0 * n_kv_tiles;
+  const int kv_head = g0 + r_in % g_heads;
+  const int slot = r_in / g_heads;
   // deterministic mode launches each head's kv tiles lightest-first: a CTA
   // only ever waits for a higher kv tile, which was launched before it
-  const int jt = p.dq_sem != nullptr ? n_kv_tiles - 1 - static_cast<int>(blockIdx.x % n_kv_tiles)
-                                     : static_cast<int>(blockIdx.x % n_kv_tiles);
+  const int jt = p.dq_sem != nullptr ? n_kv_tiles - 1 - slot : slot;
   const int group = p.h_q / p.h_kv;
   const int i0 = (p.mask == DA_MASK_DIAGONAL) ? jt : 0;
   const int n_i = n_q_tiles - i0;
   const int n_it = n_i > 0 ? group * n_i : 0;
+  if (threadIdx.x == 0) {
+    BWS_CTA_TRACE(0, bws_gtimer());
+    BWS_CTA_TRACE(2, clock64());
+  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -259,6 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
       mbar_wait(&bars->kv_full, 0);
       mbar_wait(&bars->q_full[0], 0);
+      BWS_CTA_TRACE(6, clock64());
       tc_fence_after();
       gemm_kk(tmem + kColS, k_addr, q_addr);
       mma_commit(&bars->s_full);
@@ -310,6 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       mma_commit(&bars->acc_full);
+      BWS_CTA_TRACE(7, clock64());
     }
   } else if (warp >= 14) {
     // idle warps of the MMA/loader warpgroup
@@ -372,7 +434,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    if (lane == 0) bulk_wait<0>();
+    // the staging boxes must outlive the TMA reads; the global adds complete
+    // on their own before the grid is considered done
+    if (lane == 0) bulk_wait_read<0>();
   } else if (warp < 4) {
     // ===================== P warps =====================
     const int quarter = warp;
@@ -426,27 +490,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (n_it > 0) {
       mbar_wait(&bars->acc_full, 0);
       tc_fence_after();
-      const int row = jt * kBN + r;
-      const bool valid = row < p.rows_kv;
-      float* dst = p.dv_acc + (static_cast<size_t>(kv_head) * p.rows_kv + row) * kHD;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t a[32];
-        tmem_ld_32x32b_x32(lane_base + kColDV + c * 32, a);
-        tmem_ld_wait();
-        if (!valid) continue;
-        float4* d4 = reinterpret_cast<float4*>(dst + c * 32);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          float4 x = make_float4(__uint_as_float(a[4 * i]), __uint_as_float(a[4 * i + 1]),
-                                 __uint_as_float(a[4 * i + 2]), __uint_as_float(a[4 * i + 3]));
-          if (p.accumulate_kv) {
-            const float4 o = d4[i];
-            x.x += o.x; x.y += o.y; x.z += o.z; x.w += o.w;
-          }
-          d4[i] = x;
-        }
-      }
+      store_acc_rows_lsu(p.dv_acc + (static_cast<size_t>(kv_head) * p.rows_kv + jt * kBN + r) * kHD,
+                         jt * kBN + r < p.rows_kv, lane_base + kColDV, 1.f, p.accumulate_kv != 0);
     } else if (p.mask != DA_MASK_EMPTY && !p.accumulate_kv) {
       // no query tile sees this kv tile: the contribution is zero
       const int row = jt * kBN + r;
@@ -526,29 +571,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (n_it > 0) {
       mbar_wait(&bars->acc_full, 0);
       tc_fence_after();
-      const int row = jt * kBN + r;
-      const bool valid = row < p.rows_kv;
-      float* dst = p.dk_acc + (static_cast<size_t>(kv_head) * p.rows_kv + row) * kHD;
-      const float f = p.scale;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t a[32];
-        tmem_ld_32x32b_x32(lane_base + kColDK + c * 32, a);
-        tmem_ld_wait();
-        if (!valid) continue;
-        float4* d4 = reinterpret_cast<float4*>(dst + c * 32);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          float4 x = make_float4(f * __uint_as_float(a[4 * i]), f * __uint_as_float(a[4 * i + 1]),
-                                 f * __uint_as_float(a[4 * i + 2]),
-                                 f * __uint_as_float(a[4 * i + 3]));
-          if (p.accumulate_kv) {
-            const float4 o = d4[i];
-            x.x += o.x; x.y += o.y; x.z += o.z; x.w += o.w;
-          }
-          d4[i] = x;
-        }
-      }
+      store_acc_rows_lsu(p.dk_acc + (static_cast<size_t>(kv_head) * p.rows_kv + jt * kBN + r) * kHD,
+                         jt * kBN + r < p.rows_kv, lane_base + kColDK, p.scale, p.accumulate_kv != 0);
     } else if (p.mask != DA_MASK_EMPTY && !p.accumulate_kv) {
       const int row = jt * kBN + r;
       if (row < p.rows_kv) {
@@ -562,6 +586,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 12) tmem_dealloc<512>(tmem);
+  if (threadIdx.x == 0) {
+    BWS_CTA_TRACE(1, bws_gtimer());
+    BWS_CTA_TRACE(3, clock64());
+    BWS_CTA_TRACE(4, bws_smid());
+    BWS_CTA_TRACE(5, static_cast<unsigned long long>(n_it));
+  }
 }
 
 }  // namespace bwdws

@@ -32,12 +32,36 @@ namespace fwd {
     if ((cond) && p.trace != nullptr && blockIdx.x == 0 && (j) < 64)            \
       p.trace[(j) * 16 + (slot)] = clock64();                                   \
   } while (0)
+// per-CTA record after the 64x16 stamps (same layout as the backward's):
+// globaltimer start/end, clock64 start/end, smid, kv tiles
+#define FWD_CTA_TRACE(slot, val)                                                \
+  do {                                                                          \
+    if (p.trace != nullptr)                                                     \
+      p.trace[1024 + static_cast<size_t>(blockIdx.x) * 8 + (slot)] = (val);     \
+  } while (0)
+__device__ __forceinline__ unsigned long long fwd_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned long long fwd_smid() {
+  uint32_t s;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+  return s;
+}
 #else
 #define FWD_TRACE(cond, j, slot) \
   do {                           \
   } while (0)
+#define FWD_CTA_TRACE(slot, val) \
+  do {                           \
+  } while (0)
 #endif
 
+#ifndef DA_FWD_HEAD_GROUP
+#define DA_FWD_HEAD_GROUP 2
+#endif
+constexpr int kHeadGroup = DA_FWD_HEAD_GROUP;
 constexpr int kBM = 128;
 constexpr int kBN = 128;
 constexpr int kHD = 128;
@@ -103,16 +127,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n_q_tiles = (p.rows_q + kBM - 1) / kBM;
   const int n_kv_tiles = (p.rows_kv + kBN - 1) / kBN;
   const int n_pairs = (n_q_tiles + 1) / 2;
-  // head-major: the co-resident CTAs share one head's K/V in L2; within a
-  // head the heaviest (latest) query pairs launch first
-  const int head = static_cast<int>(blockIdx.x / n_pairs);
-  const int pair = n_pairs - 1 - static_cast<int>(blockIdx.x % n_pairs);
+  // heads in groups of kHeadGroup: the co-resident CTAs share a group's K/V in
+  // L2; within a group the heaviest (latest) query pairs launch first, the
+  // group's heads interleaved, so the last wave is short light pairs rather
+  // than one head's long ones (head-major left a ~2% tail)
+  const int b = static_cast<int>(blockIdx.x);
+  const int g0 = (b / (kHeadGroup * n_pairs)) * kHeadGroup;
+  const int g_heads = min(kHeadGroup, p.h_q - g0);
+  const int r_in = b - g0 * n_pairs;
+  const int head = g0 + r_in % g_heads;
+  const int pair = n_pairs - 1 - r_in / g_heads;
   const int kv_head = head / (p.h_q / p.h_kv);
   const int qt0 = 2 * pair;
   const bool has_t1 = (qt0 + 1) < n_q_tiles;
   const int n0 = tiles_for(p.mask, qt0, n_kv_tiles);
   const int n1 = has_t1 ? tiles_for(p.mask, qt0 + 1, n_kv_tiles) : 0;
   const int nmax = max(n0, n1);
+  if (threadIdx.x == 0) {
+    FWD_CTA_TRACE(0, fwd_gtimer());
+    FWD_CTA_TRACE(2, clock64());
+  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -478,6 +512,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 8) tmem_dealloc<512>(tmem);
+  if (threadIdx.x == 0) {
+    FWD_CTA_TRACE(1, fwd_gtimer());
+    FWD_CTA_TRACE(3, clock64());
+    FWD_CTA_TRACE(4, fwd_smid());
+    FWD_CTA_TRACE(5, static_cast<unsigned long long>(nmax));
+    FWD_CTA_TRACE(6, 0ull);
+    FWD_CTA_TRACE(7, 0ull);
+  }
 }
 
 }  // namespace fwd
