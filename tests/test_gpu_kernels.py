@@ -213,6 +213,32 @@ def test_host_pipeline_matches_direct_calls(cuda, h, n, hpg):
     assert rel_err(torch.cat(ha.out, 0), o_ref) < TOL
 
 
+def test_host_pipeline_back_to_back_async_calls(cuda):
+    """Consecutive sync=False calls overlap (call i+1's copies of group g wait
+    only for call i's group g); each call's outputs are its own inputs' grads."""
+    from paper_2310_03294_b200 import flashcore as F
+    from paper_2310_03294_b200.pipeline import HostAttention
+    h, n = 4, 512
+    ha = HostAttention(h, n, heads_per_group=1)
+    steps = []
+    for s_ in range(3):
+        q, k, v = _qkv(h, n, seed=50 + s_)
+        do = _qkv(h, n, seed=60 + s_)[0]
+        host_in = [x.cpu().pin_memory() for x in (q, k, v, do)]
+        host_out = [torch.empty(h, n, 128, dtype=torch.bfloat16).pin_memory() for _ in range(3)]
+        ha(*host_in, *host_out, sync=False)
+        steps.append(((q, k, v, do), host_out, host_in))
+    ha.join()
+    torch.cuda.synchronize()
+    ha.check()
+    for (q, k, v, do), host_out, _ in steps:
+        out = F.block_attn_update_final(q, k, v, None, F.MaskMode.Diagonal)
+        g = F.block_attn_backward(q, k, v, out.o, out.lse, do, F.MaskMode.Diagonal)
+        assert torch.equal(host_out[1], g.dk.to(torch.bfloat16).cpu())
+        assert torch.equal(host_out[2], g.dv.to(torch.bfloat16).cpu())
+        assert rel_err(host_out[0].float(), g.dq.to(torch.bfloat16).cpu().float()) < 1e-2
+
+
 def test_host_pipeline_degenerate_rows_raise(cuda):
     """A finalize over a row that attended to no key raises DegenerateRowError
     (flashcore.hpp:233-235) even with the deferred (sync-free) flag."""

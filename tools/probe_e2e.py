@@ -21,6 +21,7 @@ for spec in (sys.argv[2] if len(sys.argv) > 2 else "2x1,2x2,4x2").split(","):
     s.record()
     for _ in range(4):
         ha(*host, *outs, sync=False)
+    ha.join()
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / 4
