@@ -256,10 +256,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row0 = cur.qt * kBM;
       mbar_wait(&bars->q_empty[st], ph ^ 1);
       if (lane == 0) {
+#ifdef DA_BWD_EXPERIMENT_NO_RELOAD  // (cost probe only: reuses stale Q/dO tiles)
+        if (it >= 2) {
+          mbar_arrive(&bars->q_full[st]);
+        } else
+#endif
+        {
         mbar_arrive_expect_tx(&bars->q_full[st], kTileBytes);
         uint8_t* qs = smem + SmemLayout::q + st * kTileBytes;
         tma_load_3d(qs, &tmap_q, &bars->q_full[st], 0, row0, hq);
         tma_load_3d(qs + kHalfTile, &tmap_q, &bars->q_full[st], 64, row0, hq);
+        }
       }
       // -lse (log2 units) and -D for the 128 query rows; padding rows get
       // -lse2 = -inf so their probabilities are exactly zero
@@ -277,9 +284,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (lane == 0) {
         mbar_wait(&bars->do_empty, (it & 1) ^ 1);
+#ifdef DA_BWD_EXPERIMENT_NO_RELOAD
+        if (it >= 1) {
+          mbar_arrive(&bars->do_full);
+        } else
+#endif
+        {
         mbar_arrive_expect_tx(&bars->do_full, kTileBytes);
         tma_load_3d(smem + SmemLayout::dout, &tmap_do, &bars->do_full, 0, row0, hq);
         tma_load_3d(smem + SmemLayout::dout + kHalfTile, &tmap_do, &bars->do_full, 64, row0, hq);
+        }
       }
       float* lse2 = vecs + st * 256;
       float* dvec = lse2 + 128;
@@ -411,14 +425,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       float* box = reinterpret_cast<float*>(smem + SmemLayout::dq_stage) + dw * 32 * 32;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
+#ifndef DA_BWD_EXPERIMENT_NO_BOX_WAIT  // (cost probe only: races on the box)
         if (lane == 0) bulk_wait_read<0>();
+#endif
         __syncwarp();
 #pragma unroll
         for (int k = 0; k < 32; ++k) box[k * 32 + lane] = p.scale * __uint_as_float(r[c][k]);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
+#if defined(DA_BWD_EXPERIMENT_DQ_STORE)  // (cost probe only: overwrites dQ)
+          tma_store_3d(&tmap_dq, box, dw * 32, row0 + c * 32, hq);
+#elif !defined(DA_BWD_EXPERIMENT_NO_DQ_REDUCE)  // (cost probe only: drops dQ)
           tma_reduce_add_3d(&tmap_dq, box, dw * 32, row0 + c * 32, hq);
+#endif
           bulk_commit();
         }
       }
