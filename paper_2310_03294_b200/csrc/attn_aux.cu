@@ -114,12 +114,14 @@ __global__ void copy_acc_kernel(const float* __restrict__ o, const float* __rest
 }
 
 int sm_count() {
-  static int n = 0;
+  static std::atomic<int> counts[64];  // per device, 0 = not queried yet
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  int n = counts[dev & 63].load(std::memory_order_relaxed);
   if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+    counts[dev & 63].store(n, std::memory_order_relaxed);
   }
   return n;
 }

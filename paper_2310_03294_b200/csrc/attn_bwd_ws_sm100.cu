@@ -619,20 +619,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 cudaError_t launch_attn_bwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                             const CUtensorMap& tdo, const CUtensorMap& tdq, const BwdParams& p,
                             cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(bwdws::attn_bwd_ws_kernel,
+  static std::atomic<uint64_t> configured{0};
+  cudaError_t e = once_per_device(configured, [] {
+    cudaError_t r = cudaFuncSetAttribute(bwdws::attn_bwd_ws_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(bwdws::kSmemBytes));
-    if (e != cudaSuccess) return e;
+    if (r != cudaSuccess) return r;
     cudaFuncAttributes attr{};
-    e = cudaFuncGetAttributes(&attr, bwdws::attn_bwd_ws_kernel);
-    if (e != cudaSuccess) return e;
+    r = cudaFuncGetAttributes(&attr, bwdws::attn_bwd_ws_kernel);
+    if (r != cudaSuccess) return r;
     // setmaxnreg redistributes a fixed CTA budget; any other launch register
     // count would make the drain warps' increase wait forever.
-    if (attr.numRegs != bwdws::kLaunchRegs) return cudaErrorInvalidConfiguration;
-    configured = true;
-  }
+    return attr.numRegs == bwdws::kLaunchRegs ? cudaSuccess : cudaErrorInvalidConfiguration;
+  });
+  if (e != cudaSuccess) return e;
   const int n_kv_tiles = (p.rows_kv + bwdws::kBN - 1) / bwdws::kBN;
   dim3 grid(n_kv_tiles * p.h_kv);
   bwdws::attn_bwd_ws_kernel<<<grid, bwdws::kThreads, bwdws::kSmemBytes, stream>>>(tq, tk, tv, tdo,

@@ -526,14 +526,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 cudaError_t launch_attn_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                             const FwdParams& p, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(fwd::attn_fwd_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(fwd::kSmemBytes));
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static std::atomic<uint64_t> configured{0};
+  cudaError_t e = once_per_device(configured, [] {
+    return cudaFuncSetAttribute(fwd::attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(fwd::kSmemBytes));
+  });
+  if (e != cudaSuccess) return e;
   const int n_q_tiles = (p.rows_q + fwd::kBM - 1) / fwd::kBM;
   const int n_pairs = (n_q_tiles + 1) / 2;
   dim3 grid(n_pairs * p.h_q);

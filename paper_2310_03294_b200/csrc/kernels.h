@@ -3,11 +3,27 @@
 
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 
 #include "../../include/distattn_b200.h"
 
 namespace da {
+
+// One-time per-device setup (function attributes, cached device queries):
+// runs `f` until it succeeds once on the current device. Thread-safe; two
+// threads racing on the first call both run the (idempotent) setup.
+template <class F>
+inline cudaError_t once_per_device(std::atomic<uint64_t>& done, F&& f) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = f();
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 struct FwdParams {
   int h_q, h_kv, rows_q, rows_kv;
