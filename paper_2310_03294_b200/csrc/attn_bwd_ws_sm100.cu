@@ -106,6 +106,7 @@ struct Bars {
   uint64_t q_full[2];
   uint64_t q_empty[2];
   uint64_t vec_full[2];
+  uint64_t vec_empty[2];  // P + dS warps (one arrive per warp) -> loader
   uint64_t do_full;
   uint64_t do_empty;
   uint64_t s_full;
@@ -191,6 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(&bars->q_full[s], 1);
         mbar_init(&bars->q_empty[s], 1);
         mbar_init(&bars->vec_full[s], 1);
+        mbar_init(&bars->vec_empty[s], 8);
       }
       mbar_init(&bars->do_full, 1);
       mbar_init(&bars->do_empty, 1);
@@ -297,6 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       float* lse2 = vecs + st * 256;
       float* dvec = lse2 + 128;
+      mbar_wait(&bars->vec_empty[st], ph ^ 1);  // iteration it-2 done reading this stage
       *reinterpret_cast<float4*>(lse2 + lane * 4) = make_float4(l2[0], l2[1], l2[2], l2[3]);
       *reinterpret_cast<float4*>(dvec + lane * 4) = make_float4(dd[0], dd[1], dd[2], dd[3]);
       __syncwarp();
@@ -501,6 +504,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // (columns [16 c, 16 c + 16): already read)
         tmem_st_32x32b_x16(s_tmem + c * 16, pk);
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->vec_empty[st]);  // lse2[st] no longer read
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&bars->p_full);
@@ -581,6 +586,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               make_uint4(dsk[4 * ch + 0], dsk[4 * ch + 1], dsk[4 * ch + 2], dsk[4 * ch + 3]);
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->vec_empty[st]);  // dvec[st] no longer read
       fence_proxy_async_smem();
       tmem_st_wait();
       tc_fence_before();

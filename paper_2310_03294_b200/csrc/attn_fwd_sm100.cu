@@ -409,9 +409,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       FWD_TRACE(quarter == 0 && lane == 0, j, 7 + 6 * t);
       l_run = l_run * alpha + rs;
 
+      // PV(j-1) is complete (S(j) was committed after it), so this wait never
+      // blocks; it consumes every o_done phase, which keeps the barrier protocol
+      // checkable (compute-sanitizer synccheck)
+      if (j > 0) mbar_wait(&bars->o_done[t], (j - 1) & 1);
       // lazy O correction: only warps with a row whose max jumped
       if (j > 0 && __any_sync(0xffffffffu, need)) {
-        mbar_wait(&bars->o_done[t], (j - 1) & 1);
         tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
