@@ -39,6 +39,12 @@ def main():
     g3 = F.block_attn_backward(q3, k3, v3, o3.o, o3.lse, do3, F.MaskMode.Full)
     F.block_attn_backward(q3, k3, v3, o3.o, o3.lse, do3, F.MaskMode.Full, grads=g3,
                           accumulate_kv=True)
+    # the native P-worker executor (schedules, message buffers, merges, split halves)
+    from paper_2310_03294_b200.runtime import make_parity_shards, run_backward, run_forward
+    for kind, bwd in (("balanced", "ring"), ("balanced_split", "balanced"), ("ring", "ring")):
+        shards = make_parity_shards(3, 4, 1024, 2, 128, heads_kv=1)
+        run_forward(shards, kind)
+        run_backward(shards, bwd)
     torch.cuda.synchronize()
     print("sanitize cases done")
 
