@@ -229,11 +229,11 @@ def run_single(args):
     def e2e_step():
         ha(hq, hk, hv, hdo, hdq, hdk, hdv, sync=False)
 
-    for _ in range(2):
+    for _ in range(max(3, args.warmup)):
         e2e_step()
     ha.join(stream)
     torch.cuda.synchronize()
-    e_steps = max(2, min(args.steps, 5))
+    e_steps = max(2, args.steps)  # the same K as the device-timed steps
     s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s2.record(stream)
     for _ in range(e_steps):
