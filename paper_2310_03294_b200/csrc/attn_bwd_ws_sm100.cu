@@ -96,10 +96,15 @@ struct SmemLayout {
   static constexpr uint32_t ds = dout + kTileBytes;     // dS^T [kv][q] bf16, SW128
   static constexpr uint32_t vecs = ds + kTileBytes;     // 2 stages x (-lse2[128], -D[128])
   static constexpr uint32_t bars = vecs + 2 * 2 * 128 * 4;
-  static constexpr uint32_t dq_stage = bars + 1024;  // 4 warps x [32 q][32 d] fp32
-  static constexpr uint32_t total = dq_stage + 4 * 32 * 32 * 4;
+  // 4 drain warps x 2 boxes of [32 q][32 d] fp32: two TMA reductions in flight
+  // per warp (the drain throughput is bounded by bytes in flight / latency)
+  static constexpr uint32_t dq_stage = bars + 256;
+  static constexpr uint32_t total = dq_stage + 4 * 2 * 32 * 32 * 4;
 };
-constexpr size_t kSmemBytes = SmemLayout::total + 1024;
+// The dynamic window starts 1024-aligned on sm_100 (after the 1 KB reserved
+// per CTA), so no alignment slack is reserved; the kernel traps if it is not.
+constexpr size_t kSmemBytes = SmemLayout::total;
+static_assert(kSmemBytes <= 232448, "dynamic shared memory per CTA");
 
 struct Bars {
   uint64_t kv_full;
@@ -119,7 +124,7 @@ struct Bars {
   uint64_t acc_full;
   uint32_t tmem_base;
 };
-static_assert(sizeof(Bars) <= 1024, "barrier block");
+static_assert(sizeof(Bars) <= 256, "barrier block");
 
 // dK/dV epilogue: each thread stores its accumulator row (TMEM lane) from
 // registers. (Staging the rows in the free smem tiles and writing them with TMA
@@ -154,8 +159,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                        const __grid_constant__ CUtensorMap tmap_do,
                        const __grid_constant__ CUtensorMap tmap_dq, const BwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-byte alignment by offsetting the __shared__ symbol (keeps LDS/STS)
-  uint8_t* smem = smem_raw + smem_align_pad(smem_raw);
+  // SW128 tiles need 1024-byte alignment: checked, not padded (see kSmemBytes)
+  if (smem_align_pad(smem_raw) != 0) __trap();  // see kSmemBytes
+  uint8_t* smem = smem_raw;
   Bars* bars = reinterpret_cast<Bars*>(smem + SmemLayout::bars);
   float* vecs = reinterpret_cast<float*>(smem + SmemLayout::vecs);
 
@@ -425,12 +431,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // stage [32 q][32 d] boxes (this warp's 32 head-dim columns) and let TMA
       // reduce them into dq_acc: no LSU atomics; OOB query rows are clipped
-      float* box = reinterpret_cast<float*>(smem + SmemLayout::dq_stage) + dw * 32 * 32;
+      float* box2 = reinterpret_cast<float*>(smem + SmemLayout::dq_stage) + dw * 2 * 32 * 32;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-#ifndef DA_BWD_EXPERIMENT_NO_BOX_WAIT  // (cost probe only: races on the box)
-        if (lane == 0) bulk_wait_read<0>();
-#endif
+        float* box = box2 + (c & 1) * 32 * 32;
+        // the reduction that last read this box was committed two groups ago
+        if (lane == 0) bulk_wait_read<1>();
         __syncwarp();
 #pragma unroll
         for (int k = 0; k < 32; ++k) box[k * 32 + lane] = p.scale * __uint_as_float(r[c][k]);
@@ -445,6 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           bulk_commit();
         }
       }
+      BWS_TRACE(dw == 0 && lane == 0, it, 10);
       if (sem != nullptr) {
         // this CTA's partial is complete in global memory: pass the turn on
         if (lane == 0) bulk_wait<0>();

@@ -24,9 +24,9 @@ for _ in range(3):
 torch.cuda.synchronize()
 t = tr.view(64, 16).cpu().tolist()
 names = ["mma:p_ok", "mma:ds_ok", "mma:drained", "P:s_ok", "P:done", "dS:dp_ok", "dS:p_read",
-         "dS:done", "drn:dq_ok", "drn:drained"]
+         "dS:done", "drn:dq_ok", "drn:drained", "drn:staged"]
 for it in range(4, 20):
     row = t[it]
     t0 = row[0]
     print(f"it {it:2d} period {t[it + 1][0] - row[0]:6d}  " +
-          " ".join(f"{names[s]}={row[s] - t0:+6d}" for s in range(1, 10)))
+          " ".join(f"{names[s]}={row[s] - t0:+6d}" for s in range(1, 11)))
