@@ -54,15 +54,59 @@ def peaks():
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
+    """SM clock + clock-event reasons sampled every ~5 ms by NVML in a thread
+    (nvidia-smi as a fallback). `timed(True/False)` brackets the timed region:
+    the summary's median covers those samples only (all samples if none)."""
     FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown," \
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
              "clocks_event_reasons.sw_power_cap"
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, index: int = 0):
+    def __init__(self, index: int = 0, period_s: float = 0.005):
         self.index = index
+        self.period = period_s
         self.proc = None
+        self.thread = None
+        self.samples = []  # (in_timed_region, sm_mhz, max_mhz, reasons)
+        self._timed = False
+        self._stop = False
+
+    def _nvml_handle(self):
+        import pynvml as N
+        N.nvmlInit()
+        try:  # match the CUDA device by PCI address (CUDA and NVML orders may differ)
+            import torch
+            p = torch.cuda.get_device_properties(self.index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            return N, N.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return N, N.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _run_nvml(self, N, h):
+        bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+        mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+        while not self._stop:
+            try:
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((self._timed, float(sm), float(mx),
+                                     {n for n, b in bits.items() if r & b}))
+            except Exception:
+                pass
+            time.sleep(self.period)
 
     def __enter__(self):
+        try:
+            import threading
+            N, h = self._nvml_handle()
+            self.thread = threading.Thread(target=self._run_nvml, args=(N, h), daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.thread = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
@@ -72,8 +116,13 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def timed(self, on: bool):
+        self._timed = on
+
     def __exit__(self, *a):
-        self.lines = []
+        self._stop = True
+        if self.thread is not None:
+            self.thread.join(timeout=2)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -81,23 +130,23 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
                 out, _ = self.proc.communicate()
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            for ln in out.splitlines():
+                parts = [p.strip() for p in ln.split(",")]
+                try:
+                    self.samples.append((False, float(parts[0]), float(parts[1]),
+                                         {n for n, v in zip(self.NAMES, parts[2:])
+                                          if v.lower() == "active"}))
+                except (ValueError, IndexError):
+                    continue
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in getattr(self, "lines", []):
-            parts = [p.strip() for p in ln.split(",")]
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except (ValueError, IndexError):
-                continue
-            for n, v in zip(names, parts[2:]):
-                if v.lower() == "active":
-                    reasons.add(n)
+        inside = [x for x in self.samples if x[0]] or self.samples
+        sm = [x[1] for x in inside]
+        mx = max((x[2] for x in self.samples), default=0.0)
+        reasons = set().union(*(x[3] for x in inside)) if inside else set()
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml" if self.thread is not None else "nvidia-smi"}
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -201,15 +250,17 @@ def run_single(args):
         return out
 
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(0) as clk:  # started before the warm-up: nvidia-smi needs ~0.2 s
+    with ClockSampler(0) as clk:  # started before the warm-up
         for _ in range(args.warmup):
             step()
         torch.cuda.synchronize()
+        clk.timed(True)
         start.record(stream)
         for _ in range(args.steps):
             step(record=True)
         end.record(stream)
         torch.cuda.synchronize()
+        clk.timed(False)
     ms = start.elapsed_time(end) / args.steps
     F.check_degenerate(dflag)
     fl = flops_fwd_bwd(n, heads)

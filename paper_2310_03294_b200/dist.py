@@ -819,16 +819,18 @@ def bench_main(args) -> int:
         _sys.path.insert(0, str(root))
     from bench import ClockSampler, peaks  # noqa: E402  (same sampler as the N=1 arm)
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:  # started before the warm-up: nvidia-smi needs ~0.2 s
+    with ClockSampler(local) as clk:  # started before the warm-up
         for _ in range(args.warmup):
             step()
         torch.cuda.synchronize()
         tdist.barrier()
+        clk.timed(True)
         s.record()
         for _ in range(args.steps):
             step()
         e.record()
         torch.cuda.synchronize()
+        clk.timed(False)
     tdist.barrier()
     ms = torch.tensor([s.elapsed_time(e) / args.steps], device=dev)
     tdist.all_reduce(ms, op=tdist.ReduceOp.MAX)
