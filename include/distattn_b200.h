@@ -286,10 +286,12 @@ da_status da_rank_backward(da_rank* r, int schedule_kind, const void* d_out, flo
 da_status da_rng_uniform(uint64_t state, int64_t n, double lo, double hi, int dtype, void* out,
                          void* stream);
 
-/* Debug: device buffer (64 x 16 uint64) receiving the backward kernel's
- * per-iteration clock64 timeline of CTA 0 in DA_TRACE builds; NULL disables. */
+/* Debug: device buffer receiving, in DA_TRACE builds only, the backward
+ * kernel's per-iteration clock64 timeline of CTA 0 (64 x 16 uint64) followed
+ * by 8 uint64 per CTA (globaltimer / clock64 start and end, SM id, iteration
+ * count, first / last MMA issue): size it 1024 + 8 * grid. NULL disables. */
 void da_debug_set_bwd_trace(void* buf);
-/* Debug: same for the forward kernel (64 x 16 uint64). */
+/* Debug: same layout for the forward kernel. */
 void da_debug_set_fwd_trace(void* buf);
 
 /* Debug: compute the raw score block S = q kᵀ (fp32, unscaled) of the first

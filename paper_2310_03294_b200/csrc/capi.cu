@@ -309,7 +309,8 @@ da_status da_convert_f32_bf16(const float* src, void* dst, int64_t n, void* stre
   return e == cudaSuccess ? DA_OK : da::cuda_error(e, "da_convert_f32_bf16");
 }
 
-// Debug (DA_TRACE builds only record): device buffer of 64*16 uint64 stamps.
+// Debug (DA_TRACE builds only record): device buffer of 64*16 uint64 per-iteration
+// stamps of CTA 0 followed by 8 uint64 per CTA (timers, SM id, iterations).
 void da_debug_set_bwd_trace(void* buf) { da::g_bwd_trace = static_cast<unsigned long long*>(buf); }
 void da_debug_set_fwd_trace(void* buf) { da::g_fwd_trace = static_cast<unsigned long long*>(buf); }
 

@@ -17,12 +17,12 @@ out = block_attn_update_final(q, k, v, None, MaskMode.Diagonal)
 dvec = backward_aux(do, out.o)
 g = ChunkGrads(torch.zeros(h, n, 128, device="cuda"), torch.empty(h, n, 128, device="cuda"),
                torch.empty(h, n, 128, device="cuda"))
-tr = torch.zeros(64 * 16, dtype=torch.int64, device="cuda")
+tr = torch.zeros(64 * 16 + 8 * h * ((n + 127) // 128), dtype=torch.int64, device="cuda")  # + per-CTA records
 _lib.lib().da_debug_set_bwd_trace(C.c_void_p(tr.data_ptr()))
 for _ in range(3):
     block_attn_backward(q, k, v, out.o, out.lse, do, MaskMode.Diagonal, d_vec=dvec, grads=g)
 torch.cuda.synchronize()
-t = tr.view(64, 16).cpu().tolist()
+t = tr[:1024].view(64, 16).cpu().tolist()
 names = ["mma:p_ok", "mma:ds_ok", "mma:drained", "P:s_ok", "P:done", "dS:dp_ok", "dS:p_read",
          "dS:done", "drn:dq_ok", "drn:drained", "drn:staged"]
 for it in range(4, 20):

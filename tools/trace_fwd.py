@@ -11,12 +11,12 @@ from paper_2310_03294_b200.flashcore import MaskMode, block_attn_update_final  #
 
 h, n = 32, int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 q, k, v = [(torch.rand(h, n, 128, device="cuda") * 2 - 1).to(torch.bfloat16) for _ in range(3)]
-tr = torch.zeros(64 * 16, dtype=torch.int64, device="cuda")
+tr = torch.zeros(64 * 16 + 8 * h * ((n + 255) // 256), dtype=torch.int64, device="cuda")  # + per-CTA records
 _lib.lib().da_debug_set_fwd_trace(C.c_void_p(tr.data_ptr()))
 for _ in range(3):
     block_attn_update_final(q, k, v, None, MaskMode.Diagonal)
 torch.cuda.synchronize()
-t = tr.view(64, 16).cpu().tolist()
+t = tr[:1024].view(64, 16).cpu().tolist()
 names = {0: "mma:loop", 1: "mma:p0_ok", 2: "mma:p1_ok"}
 for tt in range(2):
     for k, nm in enumerate(("s_ok", "ld", "max", "bar", "exp", "p_done")):
