@@ -9,11 +9,12 @@
 // Design (per CTA = one head x two 128-row query tiles "pair"):
 //   warp 0-3  softmax for query tile 0  (thread = query row = TMEM lane)
 //   warp 4-7  softmax for query tile 1
-//   warp 8    MMA issuer (one thread): S_t = Q_t K_j^T (SS), O_t += P_t V_j (TS)
-//   warp 9    TMA producer: Q once, K_j / V_j through a 2-stage ring
+//   warp 8    MMA issuer (one thread): S_t = Q_t K_j^T (SS), O_t += P_t V_j (SS)
+//   warp 9    TMA producer: Q once, K_j through a 2-stage ring, V_j single-stage
 // TMEM (512 cols): S_0 [0,128) S_1 [128,256) O_0 [256,384) O_1 [384,512);
-// P_t (bf16) aliases the upper half of S_t. The two query tiles ping-pong:
-// while softmax t works on S_t(j) the tensor core runs the other tile's MMAs.
+// P_t (bf16) is written to its own smem tile, so S_t(j+1) is computed while
+// softmax t still works on S_t(j) (it holds S_t(j) in registers). The two
+// query tiles' exponential loops ping-pong on the MUFU.
 // O is rescaled lazily (only when the running max grows by > 2^8).
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -80,17 +81,28 @@ constexpr bool kMufuPingPong = true;
 #else
 constexpr bool kMufuPingPong = false;
 #endif
+// P through shared memory (one 32 KB buffer per tile) and PV as an SS MMA:
+// S(j+1) no longer has to wait for PV(j) to consume P(j) in the S columns, so
+// a tile's next softmax follows its current one directly. The smem for the
+// two P tiles comes from a single-stage V ring.
+#ifndef DA_FWD_P_SMEM
+#define DA_FWD_P_SMEM 1
+#endif
+constexpr bool kPSmem = DA_FWD_P_SMEM != 0;
+constexpr int kVStages = kPSmem ? 1 : 2;
 
 struct SmemLayout {
   // all tiles 1024B aligned (SW128)
   static constexpr uint32_t q0 = 0;
   static constexpr uint32_t q1 = q0 + kTileBytes;
   static constexpr uint32_t k = q1 + kTileBytes;                 // kStages tiles
-  static constexpr uint32_t v = k + kStages * kTileBytes;        // kStages tiles
-  static constexpr uint32_t bars = v + kStages * kTileBytes;     // barriers
+  static constexpr uint32_t v = k + kStages * kTileBytes;        // kVStages tiles
+  static constexpr uint32_t pbuf = v + kVStages * kTileBytes;    // P_0, P_1 (kPSmem)
+  static constexpr uint32_t bars = pbuf + (kPSmem ? 2 * kTileBytes : 0);  // barriers
   static constexpr uint32_t total = bars + 256;
 };
-constexpr size_t kSmemBytes = SmemLayout::total + 1024;  // + alignment slack
+constexpr size_t kSmemBytes = SmemLayout::total + (kPSmem ? 0 : 1024);  // + alignment slack
+static_assert(kSmemBytes <= 232448, "dynamic shared memory per CTA");
 
 struct Bars {
   uint64_t q_full;
@@ -101,6 +113,7 @@ struct Bars {
   uint64_t s_full[2];
   uint64_t p_full[2];
   uint64_t o_done[2];
+  uint64_t s_free[2];     // kPSmem: softmax t holds S_t(j) in registers
   uint32_t tmem_base;
 };
 static_assert(sizeof(Bars) <= 256, "barrier block");
@@ -117,6 +130,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment (SW128) by offsetting the __shared__ symbol itself, so
   // the compiler keeps the shared address space (STS/LDS, not generic ST/LD)
+  // (kPSmem: no slack left, so the 1024-aligned window is checked instead)
+  if (kPSmem && smem_align_pad(smem_raw) != 0) __trap();
   uint8_t* smem = smem_raw + smem_align_pad(smem_raw);
   Bars* bars = reinterpret_cast<Bars*>(smem + SmemLayout::bars);
 
@@ -161,6 +176,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(&bars->s_full[t], 1);
         mbar_init(&bars->p_full[t], 128);
         mbar_init(&bars->o_done[t], 1);
+        mbar_init(&bars->s_free[t], 128);
       }
       fence_barrier_init();
     }
@@ -190,19 +206,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_3d(smem + SmemLayout::q1 + kHalfTile, &tmap_q, &bars->q_full, 64, row0 + kBM,
                     head);
       }
-      for (int j = 0; j < nmax; ++j) {
+      auto load_k = [&](int j) {
         const int s = j % kStages;
-        const uint32_t ph = (j / kStages) & 1;
         uint8_t* ks = smem + SmemLayout::k + s * kTileBytes;
-        uint8_t* vs = smem + SmemLayout::v + s * kTileBytes;
-        mbar_wait(&bars->k_empty[s], ph ^ 1);
+        mbar_wait(&bars->k_empty[s], ((j / kStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&bars->k_full[s], kTileBytes);
         tma_load_3d(ks, &tmap_k, &bars->k_full[s], 0, j * kBN, kv_head);
         tma_load_3d(ks + kHalfTile, &tmap_k, &bars->k_full[s], 64, j * kBN, kv_head);
-        mbar_wait(&bars->v_empty[s], ph ^ 1);
+      };
+      auto load_v = [&](int j) {
+        const int s = j % kVStages;
+        uint8_t* vs = smem + SmemLayout::v + s * kTileBytes;
+        mbar_wait(&bars->v_empty[s], ((j / kVStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&bars->v_full[s], kTileBytes);
         tma_load_3d(vs, &tmap_v, &bars->v_full[s], 0, j * kBN, kv_head);
         tma_load_3d(vs + kHalfTile, &tmap_v, &bars->v_full[s], 64, j * kBN, kv_head);
+      };
+      for (int j = 0; j < nmax; ++j) {
+        if (kPSmem) {
+          // K runs a tile ahead of V (the single V stage frees only after both PVs)
+          if (j == 0) load_k(0);
+          if (j + 1 < nmax) load_k(j + 1);
+        } else {
+          load_k(j);
+        }
+        load_v(j);
       }
     }
   } else if (warp == 8) {
@@ -230,10 +258,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t vb = v_addr + stage * kTileBytes;
         const uint32_t d_tmem = tmem + 256 + t * 128;
         const uint32_t p_tmem = tmem + t * 128 + 64;
+        const uint32_t p_addr = smem_u32(smem + SmemLayout::pbuf) + t * kTileBytes;
 #pragma unroll
         for (int kk = 0; kk < kBN / 16; ++kk) {
           const uint64_t b = make_sdesc_sw128(vb + kk * 2048, kHalfTile, 1024);
-          mma_ts(d_tmem, p_tmem + kk * 8, b, idesc_pv, (acc || kk > 0) ? 1u : 0u);
+          if (kPSmem) {
+            const uint32_t off = (kk >> 2) * kHalfTile + (kk & 3) * 32;
+            mma_ss(d_tmem, make_sdesc_sw128(p_addr + off, 16, 1024), b, idesc_pv,
+                   (acc || kk > 0) ? 1u : 0u);
+          } else {
+            mma_ts(d_tmem, p_tmem + kk * 8, b, idesc_pv, (acc || kk > 0) ? 1u : 0u);
+          }
         }
       };
 
@@ -249,7 +284,38 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mma_commit(&bars->k_empty[0]);
       }
-      for (int j = 0; j < nmax; ++j) {
+      for (int j = 0; kPSmem && j < nmax; ++j) {
+        const bool has_next = j + 1 < nmax;
+        const int s1 = (j + 1) % kStages;
+        const uint32_t ph1 = ((j + 1) / kStages) & 1;
+        FWD_TRACE(true, j, 0);
+        // S_t(j+1) as soon as softmax t holds S_t(j) in registers
+        if (has_next) {
+          mbar_wait(&bars->k_full[s1], ph1);
+          for (int t = 0; t < 2; ++t) {
+            if (j + 1 < n_t[t]) {
+              mbar_wait(&bars->s_free[t], j & 1);
+              tc_fence_after();
+              issue_s(t, s1);
+              mma_commit(&bars->s_full[t]);
+            }
+          }
+          mma_commit(&bars->k_empty[s1]);
+        }
+        // PV_t(j) once P_t(j) is in its shared buffer
+        mbar_wait(&bars->v_full[0], j & 1);
+        for (int t = 0; t < 2; ++t) {
+          if (j < n_t[t]) {
+            mbar_wait(&bars->p_full[t], j & 1);
+            FWD_TRACE(true, j, 1 + t);
+            tc_fence_after();
+            issue_pv(t, 0, j > 0);
+            mma_commit(&bars->o_done[t]);
+          }
+        }
+        mma_commit(&bars->v_empty[0]);
+      }
+      for (int j = 0; !kPSmem && j < nmax; ++j) {
         const int s = j % kStages;
         const uint32_t ph = (j / kStages) & 1;
         const bool has_next = j + 1 < nmax;
@@ -302,6 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef DA_FWD_EXPERIMENT_MMA_ONLY  // (cost probe only: no softmax, garbage output)
       if (j > 0) mbar_wait(&bars->o_done[t], (j - 1) & 1);
       tc_fence_before();
+      if (kPSmem && j + 1 < n_tiles) mbar_arrive(&bars->s_free[t]);
       mbar_arrive(&bars->p_full[t]);
       l_run = 1.f;
       continue;
@@ -310,6 +377,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(s_tmem + c * 32, sr[c]);
       tmem_ld_wait();
+      if (kPSmem && j + 1 < n_tiles) {
+        tc_fence_before();
+        mbar_arrive(&bars->s_free[t]);  // S_t(j+1) may overwrite the S columns
+      }
       FWD_TRACE(quarter == 0 && lane == 0, j, 4 + 6 * t);
 
       if (p.debug_s != nullptr && j == 0 && t == 0 && blockIdx.x == 0) {
@@ -418,9 +489,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       FWD_TRACE(quarter == 0 && lane == 0, j, 7 + 6 * t);
       l_run = l_run * alpha + rs;
 
-      // PV(j-1) is complete (S(j) was committed after it), so this wait never
-      // blocks; it consumes every o_done phase, which keeps the barrier protocol
-      // checkable (compute-sanitizer synccheck)
+      // PV(j-1) complete: O may be corrected and (kPSmem) P_t(j-1)'s buffer is
+      // free. Without kPSmem it never blocks (S(j) was committed after it).
+      // Waited every iteration, which keeps the protocol checkable (synccheck).
       if (j > 0) mbar_wait(&bars->o_done[t], (j - 1) & 1);
       // lazy O correction: only warps with a row whose max jumped
       if (j > 0 && __any_sync(0xffffffffu, need)) {
@@ -436,9 +507,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
 
-      tmem_st_32x32b_x32(p_tmem, pk[0]);
-      tmem_st_32x32b_x32(p_tmem + 32, pk[1]);
-      tmem_st_wait();
+      if (kPSmem) {
+        // P_t(j-1) was consumed: PV_t(j-1) completed (o_done waited above).
+        // K-major SW128 tile [128 q][128 kv] bf16 as two 64-column boxes
+        uint8_t* prow = smem + SmemLayout::pbuf + t * kTileBytes + row_in_tile * 128;
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch)
+            *reinterpret_cast<uint4*>(prow + b * kHalfTile + ((ch ^ (row_in_tile & 7)) * 16)) =
+                make_uint4(pk[b][4 * ch], pk[b][4 * ch + 1], pk[b][4 * ch + 2], pk[b][4 * ch + 3]);
+        fence_proxy_async_smem();
+        tmem_st_wait();  // the O correction, if any
+      } else {
+        tmem_st_32x32b_x32(p_tmem, pk[0]);
+        tmem_st_32x32b_x32(p_tmem + 32, pk[1]);
+        tmem_st_wait();
+      }
 
       tc_fence_before();
       mbar_arrive(&bars->p_full[t]);
