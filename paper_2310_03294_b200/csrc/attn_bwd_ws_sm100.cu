@@ -408,6 +408,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int hq = cur.hq;
       const int row0 = cur.qt * kBM;
       mbar_wait(&bars->dq_full, it & 1);
+#ifdef DA_BWD_EXPERIMENT_MMA_ONLY  // (cost probe only: no dQ, P or dS math)
+      tc_fence_before();
+      mbar_arrive(&bars->dq_drained);
+      continue;
+#endif
       BWS_TRACE(dw == 0 && lane == 0, it, 8);
       tc_fence_after();
       uint32_t r[4][32];
@@ -481,6 +486,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float* lse2 = vecs + st * 256;  // -lse * log2(e)
       mbar_wait(&bars->vec_full[st], (it >> 1) & 1);
       mbar_wait(&bars->s_full, it & 1);
+#ifdef DA_BWD_EXPERIMENT_MMA_ONLY
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->vec_empty[st]);
+      tc_fence_before();
+      mbar_arrive(&bars->p_full);
+      continue;
+#endif
       BWS_TRACE(quarter == 0 && lane == 0, it, 3);
       tc_fence_after();
 #pragma unroll
@@ -549,6 +561,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&bars->vec_full[st], (it >> 1) & 1);
       mbar_wait(&bars->p_full, it & 1);  // P(it) written (P warps)
       mbar_wait(&bars->dp_full, it & 1);
+#ifdef DA_BWD_EXPERIMENT_MMA_ONLY
+      tc_fence_before();
+      mbar_arrive(&bars->p_read);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->vec_empty[st]);
+      fence_proxy_async_smem();
+      mbar_arrive(&bars->ds_full);
+      continue;
+#endif
       BWS_TRACE(quarter == 0 && lane == 0, it, 5);
       tc_fence_after();
       // P(it) (64 packed columns) into registers, then release the S region
