@@ -73,7 +73,7 @@ __device__ __forceinline__ unsigned long long bws_smid() {
 #endif
 
 #ifndef DA_BWD_HEAD_GROUP
-#define DA_BWD_HEAD_GROUP 1
+#define DA_BWD_HEAD_GROUP 2
 #endif
 constexpr int kHeadGroup = DA_BWD_HEAD_GROUP;
 constexpr int kBM = 128;  // query rows per iteration
