@@ -10,7 +10,7 @@
 //   warp 0-3  softmax for query tile 0  (thread = query row = TMEM lane)
 //   warp 4-7  softmax for query tile 1
 //   warp 8    MMA issuer (one thread): S_t = Q_t K_j^T (SS), O_t += P_t V_j (SS)
-//   warp 9    TMA producer: Q once, K_j through a 2-stage ring, V_j single-stage
+//   warp 9    TMA producer: Q once, K_j single-stage, V_j through a 2-stage ring
 // TMEM (512 cols): S_0 [0,128) S_1 [128,256) O_0 [256,384) O_1 [384,512);
 // P_t (bf16) is written to its own smem tile, so S_t(j+1) is computed while
 // softmax t still works on S_t(j) (it holds S_t(j) in registers). The two
@@ -89,14 +89,21 @@ constexpr bool kMufuPingPong = false;
 #define DA_FWD_P_SMEM 1
 #endif
 constexpr bool kPSmem = DA_FWD_P_SMEM != 0;
-constexpr int kVStages = kPSmem ? 1 : 2;
+// With P in smem one K or V stage has to go: K single-stage (refilled once
+// both tiles' S(j) are done) and V double-stage measured marginally ahead of
+// the opposite split (7.85 vs 7.88 ms in the sustained step).
+#ifndef DA_FWD_K_STAGES
+#define DA_FWD_K_STAGES 1
+#endif
+constexpr int kKStages = kPSmem ? DA_FWD_K_STAGES : 2;
+constexpr int kVStages = kPSmem ? 3 - kKStages : 2;
 
 struct SmemLayout {
   // all tiles 1024B aligned (SW128)
   static constexpr uint32_t q0 = 0;
   static constexpr uint32_t q1 = q0 + kTileBytes;
   static constexpr uint32_t k = q1 + kTileBytes;                 // kStages tiles
-  static constexpr uint32_t v = k + kStages * kTileBytes;        // kVStages tiles
+  static constexpr uint32_t v = k + kKStages * kTileBytes;       // kVStages tiles
   static constexpr uint32_t pbuf = v + kVStages * kTileBytes;    // P_0, P_1 (kPSmem)
   static constexpr uint32_t bars = pbuf + (kPSmem ? 2 * kTileBytes : 0);  // barriers
   static constexpr uint32_t total = bars + 256;
@@ -207,9 +214,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     head);
       }
       auto load_k = [&](int j) {
-        const int s = j % kStages;
+        const int s = j % kKStages;
         uint8_t* ks = smem + SmemLayout::k + s * kTileBytes;
-        mbar_wait(&bars->k_empty[s], ((j / kStages) & 1) ^ 1);
+        mbar_wait(&bars->k_empty[s], ((j / kKStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&bars->k_full[s], kTileBytes);
         tma_load_3d(ks, &tmap_k, &bars->k_full[s], 0, j * kBN, kv_head);
         tma_load_3d(ks + kHalfTile, &tmap_k, &bars->k_full[s], 64, j * kBN, kv_head);
@@ -223,14 +230,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_3d(vs + kHalfTile, &tmap_v, &bars->v_full[s], 64, j * kBN, kv_head);
       };
       for (int j = 0; j < nmax; ++j) {
-        if (kPSmem) {
+        if (kPSmem && kKStages == 1) {
+          // V(j) first (its stage frees early), then K(j+1) once S(j) is done
+          if (j == 0) load_k(0);
+          load_v(j);
+          if (j + 1 < nmax) load_k(j + 1);
+        } else if (kPSmem) {
           // K runs a tile ahead of V (the single V stage frees only after both PVs)
           if (j == 0) load_k(0);
           if (j + 1 < nmax) load_k(j + 1);
+          load_v(j);
         } else {
           load_k(j);
+          load_v(j);
         }
-        load_v(j);
       }
     }
   } else if (warp == 8) {
@@ -286,8 +299,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       for (int j = 0; kPSmem && j < nmax; ++j) {
         const bool has_next = j + 1 < nmax;
-        const int s1 = (j + 1) % kStages;
-        const uint32_t ph1 = ((j + 1) / kStages) & 1;
+        const int s1 = (j + 1) % kKStages;
+        const uint32_t ph1 = ((j + 1) / kKStages) & 1;
         FWD_TRACE(true, j, 0);
         // S_t(j+1) as soon as softmax t holds S_t(j) in registers
         if (has_next) {
@@ -303,17 +316,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_commit(&bars->k_empty[s1]);
         }
         // PV_t(j) once P_t(j) is in its shared buffer
-        mbar_wait(&bars->v_full[0], j & 1);
+        const int sv = j % kVStages;
+        mbar_wait(&bars->v_full[sv], (j / kVStages) & 1);
         for (int t = 0; t < 2; ++t) {
           if (j < n_t[t]) {
             mbar_wait(&bars->p_full[t], j & 1);
             FWD_TRACE(true, j, 1 + t);
             tc_fence_after();
-            issue_pv(t, 0, j > 0);
+            issue_pv(t, sv, j > 0);
             mma_commit(&bars->o_done[t]);
           }
         }
-        mma_commit(&bars->v_empty[0]);
+        mma_commit(&bars->v_empty[sv]);
       }
       for (int j = 0; !kPSmem && j < nmax; ++j) {
         const int s = j % kStages;
