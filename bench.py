@@ -359,7 +359,7 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seq", type=int, default=SEQ)
     ap.add_argument("--heads", type=int, default=H)
-    ap.add_argument("--heads-per-group", type=int, default=1)
+    ap.add_argument("--heads-per-group", type=int, default=2)  # e2e copy/compute granularity (A/B: 2 >= 1 by ~0.5-1%)
     ap.add_argument("--fwd-schedule", default="balanced", choices=["ring", "balanced", "balanced_split"])
     ap.add_argument("--bwd-schedule", default="balanced", choices=["ring", "balanced"])
     ap.add_argument("--runtime", default="native", choices=["native", "python"],
