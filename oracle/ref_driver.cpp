@@ -272,7 +272,7 @@ int main(int argc, char** argv) {
           std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       const double flops = 7.0 * static_cast<double>(N) * N * D * H;
       std::printf("{\"seconds\":%.6f,\"flops\":%.6e,\"tflops\":%.6e,\"threads\":%d}\n", secs,
-                  flops, flops / secs / 1e12, std::min(threads, par * P));
+                  flops, flops / secs / 1e12, std::min(H, par) * P);  // threads actually running
       return 0;
     }
     std::cerr << "unknown mode " << mode << "\n";

@@ -7,6 +7,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "capi_internal.h"
@@ -83,25 +85,34 @@ static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 unsigned long long* g_bwd_trace = nullptr;
 
 // Semaphores of the deterministic dQ order: one int per (query head, query
-// tile), zeroed before every deterministic launch. Grown on demand, cached
-// per thread (allocation happens once per shape, not per call).
+// tile), zeroed before every deterministic launch. One buffer PER STREAM
+// (launches on one stream are serialised, so a reset can never overlap a
+// kernel still spinning on the same counters; launches on different streams
+// get different buffers). Growth is stream-ordered (cudaMallocAsync /
+// cudaFreeAsync on that stream), so no in-flight launch loses its buffer.
 struct SemBuffer {
   int* ptr = nullptr;
   size_t n = 0;
-  ~SemBuffer() {
-    if (ptr) cudaFree(ptr);
-  }
-  cudaError_t ensure(size_t want) {
-    if (want <= n) return cudaSuccess;
-    if (ptr) cudaFree(ptr);
-    ptr = nullptr;
-    n = 0;
-    cudaError_t e = cudaMalloc(&ptr, want * sizeof(int));
-    if (e == cudaSuccess) n = want;
-    return e;
-  }
 };
-thread_local SemBuffer g_dq_sem;
+std::mutex g_sem_mu;
+std::map<cudaStream_t, SemBuffer> g_dq_sem;
+
+cudaError_t dq_semaphores(cudaStream_t st, size_t want, int** out) {
+  std::lock_guard<std::mutex> lock(g_sem_mu);
+  SemBuffer& b = g_dq_sem[st];
+  if (want > b.n) {
+    if (b.ptr) cudaFreeAsync(b.ptr, st);
+    b.ptr = nullptr;
+    b.n = 0;
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, want * sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    b.ptr = static_cast<int*>(p);
+    b.n = want;
+  }
+  *out = b.ptr;
+  return cudaMemsetAsync(b.ptr, 0, want * sizeof(int), st);
+}
 unsigned long long* g_fwd_trace = nullptr;
 
 }  // namespace da
@@ -293,10 +304,10 @@ da_status da_attn_bwd_chunk(const da_bwd_args* a, void* stream) {
   p.dq_sem = nullptr;
   if (a->deterministic) {
     const size_t n_sem = static_cast<size_t>(a->h_q) * ((a->rows_q + 127) / 128);
-    cudaError_t e = da::g_dq_sem.ensure(n_sem);
-    if (e == cudaSuccess) e = cudaMemsetAsync(da::g_dq_sem.ptr, 0, n_sem * sizeof(int), st);
+    int* sem = nullptr;
+    cudaError_t e = da::dq_semaphores(st, n_sem, &sem);
     if (e != cudaSuccess) return da::cuda_error(e, "block_attn_backward deterministic workspace");
-    p.dq_sem = da::g_dq_sem.ptr;
+    p.dq_sem = sem;
   }
   p.trace = da::g_bwd_trace;
   cudaError_t e = da::launch_attn_bwd(tq, tk, tv, tdo, tdq, p, st);

@@ -60,12 +60,15 @@ struct PubRecord {
 struct Buf {
   void* p = nullptr;
   size_t bytes = 0;
-  void ensure(size_t b) {
-    if (b <= bytes) return;
+  // grows the buffer; callers check the status (DA_ERR_CUDA on OOM, never a null kernel arg)
+  cudaError_t ensure(size_t b) {
+    if (b <= bytes) return cudaSuccess;
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
-    if (cudaMalloc(&p, b) == cudaSuccess) bytes = b;
+    const cudaError_t e = cudaMalloc(&p, b);
+    if (e == cudaSuccess) bytes = b;
+    return e;
   }
   ~Buf() {
     if (p) cudaFree(p);
@@ -405,24 +408,24 @@ da_status da_rank_forward(da_rank* r, int schedule_kind, const void* q, const vo
   const int64_t nq = h_q * rows, nkv = h_kv * rows;
   const size_t acc_f = static_cast<size_t>(nq) * 130;  // o | m | l
   const size_t kv_b = static_cast<size_t>(nkv) * 256, q_b = static_cast<size_t>(nq) * 256;
-  r->acc.ensure(acc_f * 4);
-  r->part.ensure(acc_f * 4);
+  DA_TRY(ck(r->acc.ensure(acc_f * 4), "da_rank workspace"));
+  DA_TRY(ck(r->part.ensure(acc_f * 4), "da_rank workspace"));
   for (int i = 0; i < 2; ++i) {
-    r->kv_slot[i].ensure(2 * kv_b);
-    r->q_slot[i].ensure(q_b);
+    DA_TRY(ck(r->kv_slot[i].ensure(2 * kv_b), "da_rank workspace"));
+    DA_TRY(ck(r->q_slot[i].ensure(q_b), "da_rank workspace"));
   }
-  r->flag.ensure(sizeof(int));
-  if (!r->acc.p || !r->part.p || !r->kv_slot[1].p || !r->q_slot[1].p || !r->flag.p)
-    return set_error(DA_ERR_CUDA, "da_rank_forward: workspace allocation failed");
+  DA_TRY(ck(r->flag.ensure(sizeof(int)), "da_rank workspace"));
   const int64_t lo = rows / 2, hi = rows - lo;
   bool split = false;
   for (const Plan& p : plans) split = split || p.part != kPartWhole || !p.kvh_sends.empty();
   if (split) {
-    r->k_lo.ensure(static_cast<size_t>(h_kv) * (lo > 0 ? lo : 1) * 256);
-    r->v_lo.ensure(static_cast<size_t>(h_kv) * (lo > 0 ? lo : 1) * 256);
-    r->k_hi.ensure(static_cast<size_t>(h_kv) * hi * 256);
-    r->v_hi.ensure(static_cast<size_t>(h_kv) * hi * 256);
-    r->kvh.ensure(2 * static_cast<size_t>(h_kv) * hi * 256);
+    DA_TRY(ck(r->k_lo.ensure(static_cast<size_t>(h_kv) * (lo > 0 ? lo : 1) * 256),
+       "da_rank workspace"));
+    DA_TRY(ck(r->v_lo.ensure(static_cast<size_t>(h_kv) * (lo > 0 ? lo : 1) * 256),
+       "da_rank workspace"));
+    DA_TRY(ck(r->k_hi.ensure(static_cast<size_t>(h_kv) * hi * 256), "da_rank workspace"));
+    DA_TRY(ck(r->v_hi.ensure(static_cast<size_t>(h_kv) * hi * 256), "da_rank workspace"));
+    DA_TRY(ck(r->kvh.ensure(2 * static_cast<size_t>(h_kv) * hi * 256), "da_rank workspace"));
     cudaError_t e = cudaSuccess;
     if (lo > 0) e = pack_rows(k, r->k_lo.p, h_kv, rows, 0, lo, st);
     if (e == cudaSuccess && lo > 0) e = pack_rows(v, r->v_lo.p, h_kv, rows, 0, lo, st);
@@ -503,7 +506,7 @@ da_status da_rank_forward(da_rank* r, int schedule_kind, const void* q, const vo
     }
     for (int hw : p.merges) {
       da::Buf& buf = r->part_recv[hw];
-      buf.ensure(acc_f * 4);
+      DA_TRY(ck(buf.ensure(acc_f * 4), "da_rank workspace"));
       Work mw;
       DA_TRY(exchange(r, {}, {{buf.p, acc_f * 4, hw - 1, kPart}}, st, &mw));
       DA_TRY(wait_work(r, &mw, st));
@@ -557,14 +560,14 @@ da_status da_rank_backward(da_rank* r, int schedule_kind, const void* d_out, flo
   const size_t kv_b = static_cast<size_t>(nkv) * 256, q_b = static_cast<size_t>(nq) * 256;
   const size_t g_kv = static_cast<size_t>(nkv) * 128 * 4, g_q = static_cast<size_t>(nq) * 128 * 4;
   const size_t bundle_b = 2 * q_b + 2 * static_cast<size_t>(nq) * 4;  // q | d_out | lse | D
-  r->d_vec.ensure(static_cast<size_t>(nq) * 4);
+  DA_TRY(ck(r->d_vec.ensure(static_cast<size_t>(nq) * 4), "da_rank workspace"));
   for (int i = 0; i < 2; ++i) {
-    r->kv_slot[i].ensure(2 * kv_b);
-    r->bundle[i].ensure(bundle_b);
-    r->g_send[i].ensure(2 * g_kv);
-    r->q_send[i].ensure(g_q);
+    DA_TRY(ck(r->kv_slot[i].ensure(2 * kv_b), "da_rank workspace"));
+    DA_TRY(ck(r->bundle[i].ensure(bundle_b), "da_rank workspace"));
+    DA_TRY(ck(r->g_send[i].ensure(2 * g_kv), "da_rank workspace"));
+    DA_TRY(ck(r->q_send[i].ensure(g_q), "da_rank workspace"));
   }
-  r->g_recv.ensure(2 * g_kv);
+  DA_TRY(ck(r->g_recv.ensure(2 * g_kv), "da_rank workspace"));
   DA_TRY(ck(cudaMemsetAsync(dq, 0, g_q, st), "dq zero"));
   DA_TRY(ck(cudaMemsetAsync(dk, 0, g_kv, st), "dk zero"));
   DA_TRY(ck(cudaMemsetAsync(dv, 0, g_kv, st), "dv zero"));
@@ -647,7 +650,7 @@ da_status da_rank_backward(da_rank* r, int schedule_kind, const void* d_out, flo
     }
     for (int hw : p.merges) {
       da::Buf& buf = r->gq_recv[hw];
-      buf.ensure(g_q);
+      DA_TRY(ck(buf.ensure(g_q), "da_rank workspace"));
       recvs.push_back({buf.p, g_q, hw - 1, gq_key});
     }
     // results leave right after their kernels; waiting also retires the send

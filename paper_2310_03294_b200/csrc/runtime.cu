@@ -13,6 +13,9 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -33,6 +36,7 @@ struct Workspace {
   size_t kv_half_bytes = 0;
   int* flag = nullptr;
   std::vector<void*> allocs;
+  cudaStream_t stream = nullptr;
 
   void release() {
     for (void* p : allocs) cudaFree(p);
@@ -47,6 +51,7 @@ struct Workspace {
 
   cudaError_t ensure(int P_, int64_t h_q_, int64_t rows_) {
     if (P_ == P && h_q_ == h_q && rows_ == rows) return cudaSuccess;
+    if (!allocs.empty()) cudaStreamSynchronize(stream);  // in-flight users of the old buffers
     release();
     const size_t acc = static_cast<size_t>(h_q_) * rows_;
     auto get = [&](size_t bytes, void** out) {
@@ -79,7 +84,19 @@ struct Workspace {
   }
 };
 
-thread_local Workspace g_ws;
+// One workspace per stream: executors on different streams (or threads) never
+// share accumulators; calls on one stream are serialised by the stream.
+// A workspace is resized only after its stream drained (ensure() below).
+std::mutex g_ws_mu;
+std::map<cudaStream_t, std::unique_ptr<Workspace>> g_ws_map;
+
+Workspace& workspace_for(cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(g_ws_mu);
+  auto& w = g_ws_map[st];
+  if (!w) w.reset(new Workspace());
+  w->stream = st;
+  return *w;
+}
 
 // Packs rows [r0, r0 + n) of every head of a bf16 [h, rows, d] chunk into a
 // contiguous [h, n, d] buffer (a strided 2-D copy: one row block per head).
@@ -161,7 +178,14 @@ using namespace da;
 
 extern "C" {
 
-void da_runtime_release(void) { g_ws.release(); }
+void da_runtime_release(void) {
+  std::lock_guard<std::mutex> lock(g_ws_mu);
+  for (auto& kv : g_ws_map) {
+    cudaStreamSynchronize(kv.first);
+    kv.second->release();
+  }
+  g_ws_map.clear();
+}
 
 da_status da_run_forward(const da_shards* s, int schedule_kind, da_counters* counters,
                          void* stream) {
@@ -179,6 +203,7 @@ da_status da_run_forward(const da_shards* s, int schedule_kind, da_counters* cou
     return set_error(DA_ERR_SCHEDULE, "invalid schedule: " + errs.front() + " (" +
                                           std::to_string(errs.size()) + " violations)");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Workspace& g_ws = workspace_for(st);
   cudaError_t e = g_ws.ensure(P, s->h_q, s->rows);
   if (e != cudaSuccess) return cuda_error(e, "run_forward workspace");
 
@@ -311,6 +336,7 @@ da_status da_run_backward_sched(const da_shards* s, int schedule_kind, da_counte
     return set_error(DA_ERR_SCHEDULE, "invalid schedule: " + errs.front() + " (" +
                                           std::to_string(errs.size()) + " violations)");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Workspace& g_ws = workspace_for(st);
   cudaError_t e = g_ws.ensure(P, s->h_q, s->rows);
   if (e != cudaSuccess) return cuda_error(e, "run_backward workspace");
   const int64_t q_elems = s->h_q * s->rows * 128;

@@ -651,8 +651,10 @@ class DistRuntime:
         h, rows, d = q.shape
         hk = k.shape[0]
         be, tr = self.backend, self.transport
-        sched = (build_balanced_backward_schedule(P) if schedule == "balanced"
-                 else build_ring_backward_schedule(P))
+        builders = {"balanced": build_balanced_backward_schedule, "ring": build_ring_backward_schedule}
+        if schedule not in builders:
+            raise ConfigError(f"unknown backward schedule {schedule!r}")
+        sched = builders[schedule](P)
         viol = validate_backward(sched)
         if viol:
             raise ScheduleError(f"invalid schedule: {viol[0]} ({len(viol)} violations)")

@@ -76,10 +76,40 @@ def _req(t: torch.Tensor, dtype, name: str):
                         f"on {t.device} (contiguous={t.is_contiguous()})")
 
 
+def _shape_error(msg: str):
+    from .errors import ShapeError
+    raise ShapeError(msg)
+
+
+def _check_qkv(q, k, v, op: str):
+    """flashcore.hpp:143-147 / 284-287: the reference's operand checks, done
+    before any pointer reaches the C ABI (which cannot see tensor shapes: a
+    mismatch there would be an out-of-bounds device access, not an error)."""
+    for t, n in ((q, "q"), (k, "k"), (v, "v")):
+        _req(t, torch.bfloat16, n)
+        if t.dim() != 3:
+            _shape_error(f"{op}: {n} must be [heads, rows, d]")
+    if not (q.shape[2] == k.shape[2] == v.shape[2]):
+        _shape_error(f"{op}: hidden dims disagree")
+    if k.shape[1] != v.shape[1] or k.shape[0] != v.shape[0]:
+        _shape_error(f"{op}: k/v row mismatch")
+
+
+def _check_acc(acc: "AttnAccumulator", h_q: int, rows_q: int, d: int, op: str):
+    for t, shape in ((acc.o, (h_q, rows_q, d)), (acc.m, (h_q, rows_q)), (acc.l, (h_q, rows_q))):
+        _req(t, torch.float32, "accumulator")
+        if tuple(t.shape) != shape:
+            _shape_error(f"{op}: accumulator shape mismatch")
+
+
 def _fwd(q, k, v, acc_in, mask, scale, finalize, acc_out=None, stream=None, degenerate_flag=None):
-    _req(q, torch.bfloat16, "q"); _req(k, torch.bfloat16, "k"); _req(v, torch.bfloat16, "v")
+    _check_qkv(q, k, v, "block_attn_update")
     h_q, rows_q, d = q.shape
     h_kv, rows_kv, _ = k.shape
+    if acc_in is not None:
+        _check_acc(acc_in, h_q, rows_q, d, "block_attn_update")
+    if acc_out is not None:
+        _check_acc(acc_out, h_q, rows_q, d, "block_attn_update")
     a = _lib.FwdArgs()
     a.q, a.k, a.v = _ptr(q), _ptr(k), _ptr(v)
     a.h_q, a.h_kv, a.rows_q, a.rows_kv, a.d = h_q, h_kv, rows_q, rows_kv, d
@@ -141,9 +171,12 @@ def rescale(a: AttnAccumulator, b: AttnAccumulator, *, out: AttnAccumulator | No
             stream=None) -> AttnAccumulator:
     """flashcore.hpp:202-224: merge two partial accumulators over disjoint key sets."""
     if a.o.shape != b.o.shape:
-        from .errors import ShapeError
-        raise ShapeError("rescale: accumulator shapes disagree")
+        _shape_error("rescale: accumulator shapes disagree")
     h, rows, d = a.o.shape
+    _check_acc(a, h, rows, d, "rescale")
+    _check_acc(b, h, rows, d, "rescale")
+    if out is not None:
+        _check_acc(out, h, rows, d, "rescale")
     if out is None:
         out = AttnAccumulator(torch.empty_like(a.o), torch.empty_like(a.m), torch.empty_like(a.l))
     check(_lib.lib().da_attn_merge(_ptr(a.o), _ptr(a.m), _ptr(a.l), _ptr(b.o), _ptr(b.m), _ptr(b.l),
@@ -154,6 +187,7 @@ def rescale(a: AttnAccumulator, b: AttnAccumulator, *, out: AttnAccumulator | No
 def finalize(acc: AttnAccumulator, stream=None) -> AttnOutput:
     """flashcore.hpp:227-240; raises DegenerateRowError when a row absorbed no key."""
     h, rows, d = acc.o.shape
+    _check_acc(acc, h, rows, d, "finalize")
     out = AttnOutput(torch.empty(h, rows, d, dtype=torch.bfloat16, device=acc.o.device),
                      torch.empty(h, rows, dtype=torch.float32, device=acc.o.device))
     flag = torch.zeros(1, dtype=torch.int32, device=acc.o.device)
@@ -168,9 +202,8 @@ def finalize(acc: AttnAccumulator, stream=None) -> AttnOutput:
 def backward_aux(d_out: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
     """flashcore.hpp:250-261: D = rowsum(dO * O), fp32 [heads, rows]."""
     _req(d_out, torch.bfloat16, "d_out"); _req(out, torch.bfloat16, "out")
-    if d_out.shape != out.shape:
-        from .errors import ShapeError
-        raise ShapeError("backward_aux: shape mismatch")
+    if d_out.shape != out.shape or out.dim() != 3:
+        _shape_error("backward_aux: shape mismatch")
     h, rows, d = out.shape
     dvec = torch.empty(h, rows, dtype=torch.float32, device=out.device)
     check(_lib.lib().da_attn_bwd_preprocess(_ptr(d_out), _ptr(out), _ptr(dvec), h, rows, d,
@@ -189,11 +222,27 @@ def block_attn_backward(q, k, v, out, lse, d_out, mask: MaskMode, scale: float |
     computed when not supplied. deterministic=True adds the dq partials in a
     fixed order (bitwise reproducible; dk/dv always are).
     """
-    for t, n in ((q, "q"), (k, "k"), (v, "v"), (d_out, "d_out")):
-        _req(t, torch.bfloat16, n)
+    _check_qkv(q, k, v, "block_attn_backward")
+    _req(d_out, torch.bfloat16, "d_out")
     _req(lse, torch.float32, "lse")
     h_q, rows_q, d = q.shape
     h_kv, rows_kv, _ = k.shape
+    if tuple(out.shape) != (h_q, rows_q, d):
+        _shape_error("block_attn_backward: output shape mismatch")
+    if tuple(d_out.shape) != (h_q, rows_q, d):
+        _shape_error("block_attn_backward: upstream grad shape mismatch")
+    if tuple(lse.shape) != (h_q, rows_q):
+        _shape_error("block_attn_backward: logsumexp length mismatch")
+    if d_vec is not None:
+        _req(d_vec, torch.float32, "d_vec")
+        if tuple(d_vec.shape) != (h_q, rows_q):
+            _shape_error("block_attn_backward: D length mismatch")
+    if grads is not None:
+        for t, shape, n in ((grads.dq, (h_q, rows_q, d), "dq"), (grads.dk, (h_kv, rows_kv, d), "dk"),
+                            (grads.dv, (h_kv, rows_kv, d), "dv")):
+            _req(t, torch.float32, n)
+            if tuple(t.shape) != shape:
+                _shape_error(f"block_attn_backward: {n} accumulator shape mismatch")
     if d_vec is None:
         d_vec = backward_aux(d_out, out, stream)
     if grads is None:

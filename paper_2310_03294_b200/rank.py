@@ -45,6 +45,18 @@ class RankRuntime:
 
     def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
                 schedule: str = "balanced", stream=None):
+        from .errors import ConfigError, ShapeError
+        from .flashcore import _check_qkv
+        _check_qkv(q, k, v, "run_forward")
+        if q.shape[2] != 128:
+            from .errors import UnsupportedError
+            raise UnsupportedError("run_forward: d must be 128")
+        if k.shape[1] != q.shape[1]:
+            raise ShapeError("all shards must share the same q/k/v shape")
+        if q.shape[0] % k.shape[0] != 0:
+            raise ShapeError("h_q must be a positive multiple of h_kv")
+        if schedule not in _FWD:
+            raise ConfigError(f"unknown forward schedule {schedule!r}")
         h, rows, _ = q.shape
         hk = k.shape[0]
         out = torch.empty_like(q)
@@ -58,10 +70,16 @@ class RankRuntime:
         return out, lse, _counters(c)
 
     def backward(self, d_out: torch.Tensor, schedule: str = "ring", stream=None):
+        from .errors import ConfigError, ShapeError, StateError
+        from .flashcore import _req
         q, k, v, out, lse = self._saved if self._saved else (None,) * 5
         if q is None:
-            from .errors import StateError
             raise StateError("run_backward requires forward output and logsumexp")
+        _req(d_out, torch.bfloat16, "d_out")
+        if d_out.shape != q.shape:
+            raise ShapeError("block_attn_backward: upstream grad shape mismatch")
+        if schedule not in _BWD:
+            raise ConfigError(f"unknown backward schedule {schedule!r}")
         dq = torch.empty(q.shape, dtype=torch.float32, device=q.device)
         dk = torch.empty(k.shape, dtype=torch.float32, device=q.device)
         dv = torch.empty(k.shape, dtype=torch.float32, device=q.device)
