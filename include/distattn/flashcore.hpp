@@ -1,0 +1,297 @@
+// distattn/flashcore.hpp — signature-level drop-in for the reference's
+// /root/reference/proj/include/distattn/flashcore.hpp, backed by the sm_100a
+// kernels of libdistattn_b200.so.
+//
+// Same namespace (distattn), same include guard, same types and function
+// templates with the same signatures and value semantics:
+//   MaskMode / to_string / BlockConfig            flashcore.hpp:30-52
+//   AttnAccumulatorT / AttnOutputT (+ aliases)     flashcore.hpp:65-90
+//   dense_oracle                                   flashcore.hpp:92-128
+//   block_attn_update (accumulator by value)       flashcore.hpp:135-197
+//   rescale / finalize                             flashcore.hpp:202-240
+//   ChunkGradsT / backward_aux / block_attn_backward  flashcore.hpp:242-337
+// and the same error behaviour: the reference's operand checks throw
+// distattn::ShapeError with the reference's messages, a degenerate row throws
+// DegenerateRowError, bad block sizes ConfigError.
+//
+// A maintainer switches by putting this repository's include/ directory
+// BEFORE the reference's on the include path (errors.hpp, numerics.hpp,
+// schedule.hpp, runtime.hpp ... still come from the reference) and linking
+// libdistattn_b200.so: runtime.cpp and ckptplan.cpp compile unmodified
+// (tests/cpp/dropin_main.cpp builds exactly that).
+//
+// Precision is the product's (north_star): q/k/v/O/dO are rounded to bf16,
+// the accumulator and statistics to fp32, on upload; results come back as
+// the Scalar type. d must be 128 (the kernels' head dim); other widths throw
+// ConfigError. BlockConfig is validated but the GPU tiles are fixed at
+// 128 x 128 and live in TMEM / shared memory, so detail::score_alloc_hook is
+// never invoked (no host score block is ever allocated).
+#ifndef DISTATTN_FLASHCORE_HPP
+#define DISTATTN_FLASHCORE_HPP
+
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include <limits>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "../distattn_b200.h"
+#include "distattn/errors.hpp"
+#include "distattn/numerics.hpp"
+
+namespace distattn {
+
+enum class MaskMode { Diagonal, Full, Empty };
+
+inline const char* to_string(MaskMode m) {
+  switch (m) {
+    case MaskMode::Diagonal: return "diagonal";
+    case MaskMode::Full: return "full";
+    case MaskMode::Empty: return "empty";
+  }
+  return "?";
+}
+
+struct BlockConfig {
+  Index rows = 16;
+  Index cols = 16;
+
+  void check() const {
+    if (rows <= 0 || cols <= 0) throw ConfigError("block sizes must be positive");
+  }
+};
+
+namespace detail {
+inline thread_local std::function<void(Index, Index)> score_alloc_hook;
+
+/// C ABI status -> the reference's exception types (errors.hpp:12-48).
+inline void check_status(da_status s) {
+  if (s == DA_OK) return;
+  const std::string msg = da_last_error();
+  switch (s) {
+    case DA_ERR_SHAPE: throw ShapeError(msg);
+    case DA_ERR_CONFIG:
+    case DA_ERR_UNSUPPORTED: throw ConfigError(msg);
+    case DA_ERR_SCHEDULE: throw ScheduleError(msg);
+    case DA_ERR_STATE: throw StateError(msg);
+    case DA_ERR_DEGENERATE_ROW: throw DegenerateRowError(msg);
+    default: throw Error(msg);
+  }
+}
+
+inline int mask_code(MaskMode m) {
+  return m == MaskMode::Diagonal ? DA_MASK_DIAGONAL
+         : m == MaskMode::Full   ? DA_MASK_FULL
+                                 : DA_MASK_EMPTY;
+}
+
+/// Contiguous double view of an Eigen row-major matrix / vector: the data
+/// itself when Scalar is double, else a converted copy.
+template <class Scalar, class M>
+struct HostIn {
+  std::vector<double> tmp;
+  const double* p = nullptr;
+  explicit HostIn(const M& m) {
+    if constexpr (std::is_same_v<Scalar, double>) {
+      p = m.data();
+    } else {
+      tmp.assign(m.data(), m.data() + m.size());
+      p = tmp.data();
+    }
+  }
+};
+
+template <class Scalar, class M>
+struct HostOut {
+  std::vector<double> tmp;
+  M& m;
+  double* p = nullptr;
+  explicit HostOut(M& m_) : m(m_) {
+    if constexpr (std::is_same_v<Scalar, double>) {
+      p = m.data();
+    } else {
+      tmp.assign(m.data(), m.data() + m.size());
+      p = tmp.data();
+    }
+  }
+  ~HostOut() {
+    if constexpr (!std::is_same_v<Scalar, double>)
+      for (Index i = 0; i < static_cast<Index>(tmp.size()); ++i)
+        m.data()[i] = static_cast<Scalar>(tmp[i]);
+  }
+};
+}  // namespace detail
+
+template <class Scalar>
+struct AttnAccumulatorT {
+  Mat<Scalar> o;  // rows x d, unnormalised running output
+  Vec<Scalar> m;  // running row max (natural-log units of scale * q.k)
+  Vec<Scalar> l;  // running row sum
+
+  static AttnAccumulatorT fresh(Index rows, Index d) {
+    AttnAccumulatorT acc;
+    acc.o = Mat<Scalar>::Zero(rows, d);
+    acc.m = Vec<Scalar>::Constant(rows, -std::numeric_limits<Scalar>::infinity());
+    acc.l = Vec<Scalar>::Zero(rows);
+    return acc;
+  }
+
+  Index rows() const { return o.rows(); }
+  Index dim() const { return o.cols(); }
+};
+
+template <class Scalar>
+struct AttnOutputT {
+  Mat<Scalar> o;
+  Vec<Scalar> lse;
+};
+
+using AttnAccumulator = AttnAccumulatorT<double>;
+using AttnOutput = AttnOutputT<double>;
+
+/// Materialised attention over one chunk pair (causal = the Diagonal mask),
+/// computed by one forward launch with the fused finalize.
+template <class Scalar>
+AttnOutputT<Scalar> dense_oracle(const Mat<Scalar>& q, const Mat<Scalar>& k, const Mat<Scalar>& v,
+                                 bool causal, Scalar scale) {
+  detail::require(q.cols() == k.cols() && k.cols() == v.cols(),
+                  "dense_oracle: hidden dims disagree");
+  detail::require(k.rows() == v.rows(), "dense_oracle: k/v row mismatch");
+  AttnOutputT<Scalar> out;
+  out.o = Mat<Scalar>::Zero(q.rows(), v.cols());
+  out.lse = Vec<Scalar>(q.rows());
+  detail::HostIn<Scalar, Mat<Scalar>> hq(q), hk(k), hv(v);
+  {
+    detail::HostOut<Scalar, Mat<Scalar>> ho(out.o);
+    detail::HostOut<Scalar, Vec<Scalar>> hl(out.lse);
+    detail::check_status(da_host_dense_attention(hq.p, q.rows(), hk.p, hv.p, k.rows(), q.cols(),
+                                                 causal ? 1 : 0, static_cast<double>(scale), ho.p,
+                                                 hl.p));
+  }
+  return out;
+}
+
+/// One online-softmax update (the accumulator is taken by value and
+/// returned). Empty is a no-op that returns the accumulator bit-identical.
+template <class Scalar>
+AttnAccumulatorT<Scalar> block_attn_update(const Mat<Scalar>& q, const Mat<Scalar>& k,
+                                           const Mat<Scalar>& v, AttnAccumulatorT<Scalar> acc,
+                                           MaskMode mask, Scalar scale, BlockConfig blocks = {}) {
+  blocks.check();
+  detail::require(q.cols() == k.cols() && k.cols() == v.cols(),
+                  "block_attn_update: hidden dims disagree");
+  detail::require(k.rows() == v.rows(), "block_attn_update: k/v row mismatch");
+  detail::require(acc.rows() == q.rows() && acc.dim() == q.cols(),
+                  "block_attn_update: accumulator shape mismatch");
+  if (mask == MaskMode::Empty) return acc;
+  if (mask == MaskMode::Diagonal)
+    detail::require(q.rows() == k.rows(), "block_attn_update: diagonal mask needs a square chunk");
+  detail::HostIn<Scalar, Mat<Scalar>> hq(q), hk(k), hv(v);
+  {
+    detail::HostOut<Scalar, Mat<Scalar>> ho(acc.o);
+    detail::HostOut<Scalar, Vec<Scalar>> hm(acc.m), hl(acc.l);
+    detail::check_status(da_host_attn_update(hq.p, q.rows(), hk.p, hv.p, k.rows(), q.cols(), ho.p,
+                                             hm.p, hl.p, detail::mask_code(mask),
+                                             static_cast<double>(scale)));
+  }
+  return acc;
+}
+
+/// Merge of two partial accumulators over disjoint key sets.
+template <class Scalar>
+AttnAccumulatorT<Scalar> rescale(const AttnAccumulatorT<Scalar>& a,
+                                 const AttnAccumulatorT<Scalar>& b) {
+  detail::require(a.rows() == b.rows() && a.dim() == b.dim(),
+                  "rescale: accumulator shapes disagree");
+  AttnAccumulatorT<Scalar> out;
+  out.o = Mat<Scalar>(a.rows(), a.dim());
+  out.m = Vec<Scalar>(a.rows());
+  out.l = Vec<Scalar>(a.rows());
+  detail::HostIn<Scalar, Mat<Scalar>> ao(a.o), bo(b.o);
+  detail::HostIn<Scalar, Vec<Scalar>> am(a.m), al(a.l), bm(b.m), bl(b.l);
+  {
+    detail::HostOut<Scalar, Mat<Scalar>> oo(out.o);
+    detail::HostOut<Scalar, Vec<Scalar>> om(out.m), ol(out.l);
+    detail::check_status(da_host_attn_merge(ao.p, am.p, al.p, bo.p, bm.p, bl.p, oo.p, om.p, ol.p,
+                                            a.rows(), a.dim()));
+  }
+  return out;
+}
+
+/// O = o / l, lse = m + ln l; DegenerateRowError when a row saw no key.
+template <class Scalar>
+AttnOutputT<Scalar> finalize(const AttnAccumulatorT<Scalar>& acc) {
+  AttnOutputT<Scalar> out;
+  out.o = Mat<Scalar>(acc.rows(), acc.dim());
+  out.lse = Vec<Scalar>(acc.rows());
+  detail::HostIn<Scalar, Mat<Scalar>> o(acc.o);
+  detail::HostIn<Scalar, Vec<Scalar>> m(acc.m), l(acc.l);
+  {
+    detail::HostOut<Scalar, Mat<Scalar>> ho(out.o);
+    detail::HostOut<Scalar, Vec<Scalar>> hl(out.lse);
+    detail::check_status(
+        da_host_attn_finalize(o.p, m.p, l.p, acc.rows(), acc.dim(), ho.p, hl.p));
+  }
+  return out;
+}
+
+template <class Scalar>
+struct ChunkGradsT {
+  Mat<Scalar> dq, dk, dv;
+};
+using ChunkGrads = ChunkGradsT<double>;
+
+/// D = rowsum(d_out .* out).
+template <class Scalar>
+Vec<Scalar> backward_aux(const Mat<Scalar>& d_out, const Mat<Scalar>& out) {
+  detail::require(d_out.rows() == out.rows() && d_out.cols() == out.cols(),
+                  "backward_aux: shape mismatch");
+  Vec<Scalar> d(out.rows());
+  detail::HostIn<Scalar, Mat<Scalar>> hdo(d_out), ho(out);
+  {
+    detail::HostOut<Scalar, Vec<Scalar>> hd(d);
+    detail::check_status(da_host_backward_aux(hdo.p, ho.p, out.rows(), out.cols(), hd.p));
+  }
+  return d;
+}
+
+/// Gradient contributions of one (query chunk, kv chunk) pair from the
+/// GLOBAL logsumexp of the query rows.
+template <class Scalar>
+ChunkGradsT<Scalar> block_attn_backward(const Mat<Scalar>& q, const Mat<Scalar>& k,
+                                        const Mat<Scalar>& v, const Mat<Scalar>& out,
+                                        const Vec<Scalar>& lse, const Mat<Scalar>& d_out,
+                                        MaskMode mask, Scalar scale, BlockConfig blocks = {}) {
+  blocks.check();
+  detail::require(q.cols() == k.cols() && k.cols() == v.cols(),
+                  "block_attn_backward: hidden dims disagree");
+  detail::require(k.rows() == v.rows(), "block_attn_backward: k/v row mismatch");
+  detail::require(out.rows() == q.rows() && out.cols() == q.cols(),
+                  "block_attn_backward: output shape mismatch");
+  detail::require(d_out.rows() == q.rows() && d_out.cols() == q.cols(),
+                  "block_attn_backward: upstream grad shape mismatch");
+  detail::require(lse.size() == q.rows(), "block_attn_backward: logsumexp length mismatch");
+  if (mask == MaskMode::Diagonal)
+    detail::require(q.rows() == k.rows(),
+                    "block_attn_backward: diagonal mask needs a square chunk");
+  ChunkGradsT<Scalar> g;
+  g.dq = Mat<Scalar>::Zero(q.rows(), q.cols());
+  g.dk = Mat<Scalar>::Zero(k.rows(), k.cols());
+  g.dv = Mat<Scalar>::Zero(v.rows(), v.cols());
+  if (mask == MaskMode::Empty) return g;
+  detail::HostIn<Scalar, Mat<Scalar>> hq(q), hk(k), hv(v), ho(out), hdo(d_out);
+  detail::HostIn<Scalar, Vec<Scalar>> hl(lse);
+  {
+    detail::HostOut<Scalar, Mat<Scalar>> gq(g.dq), gk(g.dk), gv(g.dv);
+    detail::check_status(da_host_attn_backward(hq.p, q.rows(), hk.p, hv.p, k.rows(), q.cols(),
+                                               ho.p, hl.p, hdo.p, detail::mask_code(mask),
+                                               static_cast<double>(scale), gq.p, gk.p, gv.p));
+  }
+  return g;
+}
+
+}  // namespace distattn
+
+#endif  // DISTATTN_FLASHCORE_HPP

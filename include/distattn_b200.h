@@ -28,7 +28,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define DA_ABI_VERSION 2
+#define DA_ABI_VERSION 3
 
 typedef enum da_status {
   DA_OK = 0,
@@ -147,6 +147,45 @@ da_status da_attn_bwd_chunk(const da_bwd_args* args, void* stream);
 
 /* fp32 -> bf16 conversion of gradient accumulators (dq/dk/dv outputs). */
 da_status da_convert_f32_bf16(const float* src, void* dst, int64_t n, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Host-buffer forms (fp64, row-major, ONE head: the reference's Mat<double>
+ * per-head layout, numerics.hpp:26-32). What the signature-level drop-in
+ * include/distattn/flashcore.hpp calls, so the reference's own call sites
+ * (runtime.cpp:286-328, 605-716; ckptplan.cpp:146-155, 198-206) run on the
+ * sm_100a kernels. Operands are rounded to the product precision on upload
+ * (bf16 q/k/v/O/dO, fp32 accumulator and statistics); every call is
+ * synchronous on a per-thread stream with per-thread staging buffers that
+ * are grown once and reused (no allocation per call). d must be 128.
+ * ------------------------------------------------------------------------ */
+/* block_attn_update (flashcore.hpp:135-197): (o, m, l) updated in place; an
+ * accumulator with every m = -inf and l = 0 is AttnAccumulator::fresh. */
+da_status da_host_attn_update(const double* q, int64_t rows_q, const double* k, const double* v,
+                              int64_t rows_kv, int64_t d, double* o, double* m, double* l,
+                              int mask, double scale);
+/* rescale (flashcore.hpp:202-224); the output may alias an input. */
+da_status da_host_attn_merge(const double* o_a, const double* m_a, const double* l_a,
+                             const double* o_b, const double* m_b, const double* l_b,
+                             double* o_out, double* m_out, double* l_out, int64_t rows,
+                             int64_t d);
+/* finalize (flashcore.hpp:227-240): DA_ERR_DEGENERATE_ROW when a row has l <= 0. */
+da_status da_host_attn_finalize(const double* o, const double* m, const double* l, int64_t rows,
+                                int64_t d, double* out, double* lse);
+/* backward_aux (flashcore.hpp:250-261). */
+da_status da_host_backward_aux(const double* d_out, const double* out, int64_t rows, int64_t d,
+                               double* d_vec);
+/* block_attn_backward (flashcore.hpp:269-337): contributions dq [rows_q, d],
+ * dk / dv [rows_kv, d] (overwritten); D = rowsum(dO o O) computed inside.
+ * dq partials are added in a fixed order: bitwise reproducible. */
+da_status da_host_attn_backward(const double* q, int64_t rows_q, const double* k,
+                                const double* v, int64_t rows_kv, int64_t d, const double* out,
+                                const double* lse, const double* d_out, int mask, double scale,
+                                double* dq, double* dk, double* dv);
+/* dense_oracle (flashcore.hpp:92-128) as one chunk launch: causal needs
+ * rows_q == rows_kv (the Diagonal mask). */
+da_status da_host_dense_attention(const double* q, int64_t rows_q, const double* k,
+                                  const double* v, int64_t rows_kv, int64_t d, int causal,
+                                  double scale, double* out, double* lse);
 
 /* ------------------------------------------------------------------------
  * Schedules (schedule.hpp:21-119, schedule.cpp:60-108).

@@ -19,6 +19,9 @@ import numpy as np
 HERE = Path(__file__).resolve().parent
 LIB = HERE / "liboracle.so"
 REF_DRIVER = HERE / "_ref" / "ref_driver"
+# the same driver + unmodified reference sources compiled against the drop-in
+# include/distattn/flashcore.hpp (the reference runtime on the B200 kernels)
+DROPIN_DRIVER = HERE / "_ref" / "dropin_driver"
 
 _d = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
 _i64p = C.POINTER(C.c_int64)
@@ -248,11 +251,12 @@ def ref_available() -> bool:
 
 
 def ref_run(n: int, workers: int, heads: int, d: int, seed: int, schedule: str, bf16: bool,
-            timeout: int = 600):
-    """Runs the UNMODIFIED reference (oracle/_ref/ref_driver) and loads its outputs."""
+            timeout: int = 600, driver: Path = REF_DRIVER, executor: str = "stepper"):
+    """Runs the UNMODIFIED reference (oracle/_ref/ref_driver, or the drop-in
+    build oracle/_ref/dropin_driver) and loads its outputs."""
     with tempfile.TemporaryDirectory() as td:
-        subprocess.run([str(REF_DRIVER), "run", str(n), str(workers), str(heads), str(d), str(seed),
-                        schedule, td, "1" if bf16 else "0"], check=True, timeout=timeout)
+        subprocess.run([str(driver), "run", str(n), str(workers), str(heads), str(d), str(seed),
+                        schedule, td, "1" if bf16 else "0", executor], check=True, timeout=timeout)
         meta = json.loads(Path(td, "meta.json").read_text())
         arrs = {}
         for name in ("q", "k", "v", "d_out", "out", "lse", "dq", "dk", "dv"):

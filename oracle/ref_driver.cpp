@@ -170,6 +170,37 @@ int main(int argc, char** argv) {
       std::cout << "],\"cost\":[3.0,5.0,11.0]}\n";
       return 0;
     }
+    if (mode == "ckpt128") {
+      // the checkpointed layer pipeline at the kernels' head dim (d = 128,
+      // 256 tokens): the three plans' input gradients must be bit-identical
+      // (ckptplan.hpp:8-9); the first plan's d_input is written to OUT.
+      if (argc < 3) throw da::ConfigError("ckpt128 OUT");
+      const da::CheckpointStrategy strats[3] = {da::CheckpointStrategy::None,
+                                                 da::CheckpointStrategy::LayerBoundary,
+                                                 da::CheckpointStrategy::AttentionOutput};
+      const da::LayerPipeline pipe = da::make_pipeline(2, 256, 128, 256, 7);
+      da::Rng r(11);
+      const da::Matd x = r.matrix(256, 128, -1.0, 1.0);
+      const da::Matd g = r.matrix(256, 128, -1.0, 1.0);
+      std::vector<da::CkptRunResult> runs;
+      std::cout << "{\"counts\":[";
+      for (int i = 0; i < 3; ++i) {
+        runs.push_back(da::run_with_checkpointing(pipe, da::plan(pipe, strats[i]), x, g));
+        std::cout << (i ? "," : "") << "[";
+        for (int k = 0; k < da::kOpsPerLayer; ++k)
+          std::cout << (k ? "," : "") << runs.back().trace.counts[k];
+        std::cout << "]";
+      }
+      bool same = true;
+      for (size_t i = 1; i < runs.size(); ++i)
+        for (da::Index j = 0; j < runs[0].grads.d_input.size(); ++j)
+          same = same && runs[0].grads.d_input.data()[j] == runs[i].grads.d_input.data()[j];
+      std::vector<double> dx(runs[0].grads.d_input.data(),
+                             runs[0].grads.d_input.data() + runs[0].grads.d_input.size());
+      write_bin(argv[2], dx);
+      std::cout << "],\"bitwise_equal\":" << (same ? "true" : "false") << "}\n";
+      return 0;
+    }
     if (mode == "rng") {
       da::Rng r(0);
       std::cout << "{\"seed0_u64\":[";
@@ -188,7 +219,7 @@ int main(int argc, char** argv) {
       return 0;
     }
     if (mode == "run") {
-      if (argc < 9) throw da::ConfigError("run N P H D SEED SCHED OUTDIR [bf16]");
+      if (argc < 9) throw da::ConfigError("run N P H D SEED SCHED OUTDIR [bf16] [exec]");
       const da::Index N = std::stol(argv[2]);
       const int P = std::stoi(argv[3]);
       const int H = std::stoi(argv[4]);
@@ -197,6 +228,9 @@ int main(int argc, char** argv) {
       const std::string sched = argv[7];
       const std::string out = argv[8];
       const bool bf16 = argc > 9 && std::string(argv[9]) == "1";
+      // exec: stepper (default) | concurrent | both (run both executors and
+      // record whether every output is bit-identical, runtime.hpp:7-9)
+      const std::string exec = argc > 10 ? argv[10] : "stepper";
       da::Rng rng(seed);
       std::vector<std::vector<double>> buf(9);
       std::ofstream meta(out + "/meta.json");
@@ -205,9 +239,29 @@ int main(int argc, char** argv) {
            << ",\"heads\":[";
       for (int h = 0; h < H; ++h) {
         auto shards = make_head(P, N, D, rng, bf16);
+        auto twin = shards;
         da::RunOptions opts;
+        if (exec == "concurrent") opts.mode = da::ExecutorMode::Concurrent;
         const auto fr = da::run_forward(shards, pick(sched, P), opts);
         const auto bt = da::run_backward(shards, da::BackwardMode::Vanilla, opts);
+        bool same = true;
+        if (exec == "both") {
+          da::RunOptions copts;
+          copts.mode = da::ExecutorMode::Concurrent;
+          copts.overlap = true;
+          da::run_forward(twin, pick(sched, P), copts);
+          da::run_backward(twin, da::BackwardMode::Vanilla, copts);
+          auto eq = [](const auto& a, const auto& b) {
+            if (a.size() != b.size()) return false;
+            for (da::Index i = 0; i < a.size(); ++i)
+              if (a.data()[i] != b.data()[i]) return false;
+            return true;
+          };
+          for (int p = 0; p < P; ++p)
+            same = same && eq(shards[p].out, twin[p].out) && eq(shards[p].lse, twin[p].lse) &&
+                   eq(shards[p].dq, twin[p].dq) && eq(shards[p].dk, twin[p].dk) &&
+                   eq(shards[p].dv, twin[p].dv);
+        }
         for (const auto& s : shards) {
           const da::Matd* m[8] = {&s.q, &s.k, &s.v, &s.d_out, &s.out, &s.dq, &s.dk, &s.dv};
           const int slot[8] = {0, 1, 2, 3, 4, 6, 7, 8};
@@ -229,7 +283,8 @@ int main(int argc, char** argv) {
              << ",\"fwd_max_held\":" << fr.trace.max_remote_chunks_held
              << ",\"bwd_max_held\":" << bt.max_remote_chunks_held
              << ",\"fwd_makespan\":" << fr.trace.makespan << ",\"bwd_makespan\":"
-             << bt.makespan << "}";
+             << bt.makespan << ",\"executors_bitwise_equal\":" << (same ? "true" : "false")
+             << "}";
       }
       meta << "]}\n";
       const char* names[9] = {"q", "k", "v", "d_out", "out", "lse", "dq", "dk", "dv"};

@@ -80,6 +80,15 @@ SIGNATURES = {
     "da_debug_set_bwd_trace": (None, [vp]),
     "da_debug_set_fwd_trace": (None, [vp]),
     "da_debug_scores": (C.c_int, [vp, vp, i64, vp, vp]),
+    "da_host_attn_update": (C.c_int, [vp, i64, vp, vp, i64, i64, vp, vp, vp, C.c_int,
+                                      C.c_double]),
+    "da_host_attn_merge": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64]),
+    "da_host_attn_finalize": (C.c_int, [vp, vp, vp, i64, i64, vp, vp]),
+    "da_host_backward_aux": (C.c_int, [vp, vp, i64, i64, vp]),
+    "da_host_attn_backward": (C.c_int, [vp, i64, vp, vp, i64, i64, vp, vp, vp, C.c_int,
+                                        C.c_double, vp, vp, vp]),
+    "da_host_dense_attention": (C.c_int, [vp, i64, vp, vp, i64, i64, C.c_int, C.c_double, vp,
+                                          vp]),
 }
 
 _lib = None

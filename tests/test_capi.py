@@ -22,7 +22,7 @@ def test_library_exports_every_symbol():
     lib = _lib.lib()
     for name in declared_functions():
         assert hasattr(lib, name), name
-    assert lib.da_abi_version() == 2
+    assert lib.da_abi_version() == 3
 
 
 def test_status_maps_to_reference_exceptions():
