@@ -158,6 +158,33 @@ struct ChunkGrads {
   DeviceBuffer<float> dq, dk, dv;
 };
 
+/// Caller-owned device scratch of the flashcore calls (the D vector of
+/// backward_aux, the degenerate-row flag): grown on first use and reused, so
+/// the per-task calls the reference's runtime makes in a loop
+/// (runtime.cpp:286-328, 605-716) allocate nothing and never synchronise
+/// except where the reference's semantics require it (finalize throwing
+/// DegenerateRowError). One Workspace per stream.
+class Workspace {
+ public:
+  float* d_vec(int64_t n) {
+    if (static_cast<size_t>(n) > d_.size()) d_ = DeviceBuffer<float>(n);
+    return d_.data();
+  }
+  int* flag() {
+    if (flag_.size() == 0) flag_ = DeviceBuffer<int>(1);
+    return flag_.data();
+  }
+
+ private:
+  DeviceBuffer<float> d_;
+  DeviceBuffer<int> flag_;
+};
+
+inline void check_kv(const Chunk& k, const Chunk& v, const char* op) {
+  if (k.heads != v.heads || k.rows != v.rows)
+    throw ShapeError(std::string(op) + ": k/v row mismatch");
+}
+
 inline void fill_fwd_args(da_fwd_args& a, const Chunk& q, const Chunk& k, const Chunk& v,
                           MaskMode mask, double scale) {
   a.q = q.data;
@@ -177,8 +204,9 @@ inline void fill_fwd_args(da_fwd_args& a, const Chunk& q, const Chunk& k, const 
 inline AttnAccumulator block_attn_update(const Chunk& q, const Chunk& k, const Chunk& v,
                                          AttnAccumulator acc, MaskMode mask, double scale,
                                          cudaStream_t st) {
+  check_kv(k, v, "block_attn_update");
   if (acc.heads != q.heads || acc.rows != q.rows)
-    throw ShapeError("block_attn_update: accumulator shape disagrees with q");
+    throw ShapeError("block_attn_update: accumulator shape mismatch");
   da_fwd_args a{};
   fill_fwd_args(a, q, k, v, mask, scale);
   if (acc.fresh) {
@@ -210,21 +238,46 @@ inline AttnAccumulator rescale(const AttnAccumulator& x, const AttnAccumulator& 
   return out;
 }
 
+/// rescale into a caller-owned accumulator (no allocation; `out` may be `x`).
+inline void rescale_into(const AttnAccumulator& x, const AttnAccumulator& y, AttnAccumulator& out,
+                         cudaStream_t st) {
+  if (x.heads != y.heads || x.rows != y.rows || out.heads != x.heads || out.rows != x.rows)
+    throw ShapeError("rescale: accumulator shapes disagree");
+  if (x.fresh || y.fresh) throw StateError("rescale: materialise fresh accumulators first");
+  if (out.fresh) out.allocate();
+  out.fresh = false;
+  check(da_attn_merge(x.o.data(), x.m.data(), x.l.data(), y.o.data(), y.m.data(), y.l.data(),
+                      out.o.data(), out.m.data(), out.l.data(), x.heads, x.rows, kHeadDim, st));
+}
+
 /// finalize (flashcore.hpp:227-240): O = o / l (bf16), LSE = m + ln l;
 /// throws DegenerateRowError when a row attended to no key.
-inline AttnOutput finalize(const AttnAccumulator& acc, cudaStream_t st) {
+inline void finalize_into(const AttnAccumulator& acc, AttnOutput& out, Workspace& ws,
+                          cudaStream_t st) {
   if (acc.fresh) throw DegenerateRowError("finalize: a row attended to no key");
-  AttnOutput out;
+  if (out.o.size() != static_cast<size_t>(acc.heads * acc.rows * kHeadDim) ||
+      out.lse.size() != static_cast<size_t>(acc.heads * acc.rows))
+    throw ShapeError("finalize: output shape mismatch");
   out.heads = acc.heads;
   out.rows = acc.rows;
+  int* flag = ws.flag();
+  check_cuda(cudaMemsetAsync(flag, 0, sizeof(int), st), "finalize flag");
+  check(da_attn_finalize(acc.o.data(), acc.m.data(), acc.l.data(), out.o.data(), out.lse.data(),
+                         flag, acc.heads, acc.rows, kHeadDim, st));
+  check(da_check_degenerate(flag, st));  // DegenerateRowError needs the flag on the host
+}
+
+inline AttnOutput finalize(const AttnAccumulator& acc, Workspace& ws, cudaStream_t st) {
+  AttnOutput out;
   out.o = DeviceBuffer<bf16_t>(acc.heads * acc.rows * kHeadDim);
   out.lse = DeviceBuffer<float>(acc.heads * acc.rows);
-  DeviceBuffer<int> flag(1);
-  check_cuda(cudaMemsetAsync(flag.data(), 0, sizeof(int), st), "finalize flag");
-  check(da_attn_finalize(acc.o.data(), acc.m.data(), acc.l.data(), out.o.data(), out.lse.data(),
-                         flag.data(), acc.heads, acc.rows, kHeadDim, st));
-  check(da_check_degenerate(flag.data(), st));
+  finalize_into(acc, out, ws, st);
   return out;
+}
+
+inline AttnOutput finalize(const AttnAccumulator& acc, cudaStream_t st) {
+  thread_local Workspace ws;  // one flag per thread, reused
+  return finalize(acc, ws, st);
 }
 
 /// backward_aux (flashcore.hpp:250-261): D = rowsum(dO o O).
@@ -234,24 +287,33 @@ inline DeviceBuffer<float> backward_aux(const Chunk& d_out, const Chunk& out, cu
   return d;
 }
 
-/// block_attn_backward (flashcore.hpp:269-337): gradient contributions of one
-/// (query chunk, kv chunk) pair, from the GLOBAL logsumexp.
-inline ChunkGrads block_attn_backward(const Chunk& q, const Chunk& k, const Chunk& v,
-                                      const Chunk& out, const float* lse, const Chunk& d_out,
-                                      MaskMode mask, double scale, cudaStream_t st,
-                                      bool deterministic = false) {
-  ChunkGrads g{DeviceBuffer<float>(q.heads * q.rows * kHeadDim),
-               DeviceBuffer<float>(k.heads * k.rows * kHeadDim),
-               DeviceBuffer<float>(k.heads * k.rows * kHeadDim)};
-  check_cuda(cudaMemsetAsync(g.dq.data(), 0, g.dq.size() * sizeof(float), st), "dq zero");
-  DeviceBuffer<float> d = backward_aux(d_out, out, st);
+/// block_attn_backward (flashcore.hpp:269-337) into caller-owned fp32
+/// gradients: dq is accumulated into g.dq, dk / dv are added
+/// (accumulate_kv) or overwritten. D goes to the workspace; nothing is
+/// allocated and the stream is not synchronised.
+inline void block_attn_backward_into(const Chunk& q, const Chunk& k, const Chunk& v,
+                                     const Chunk& out, const float* lse, const Chunk& d_out,
+                                     MaskMode mask, double scale, ChunkGrads& g, Workspace& ws,
+                                     cudaStream_t st, bool accumulate_kv = false,
+                                     bool deterministic = false) {
+  check_kv(k, v, "block_attn_backward");
+  if (out.heads != q.heads || out.rows != q.rows)
+    throw ShapeError("block_attn_backward: output shape mismatch");
+  if (d_out.heads != q.heads || d_out.rows != q.rows)
+    throw ShapeError("block_attn_backward: upstream grad shape mismatch");
+  if (g.dq.size() != static_cast<size_t>(q.heads * q.rows * kHeadDim) ||
+      g.dk.size() != static_cast<size_t>(k.heads * k.rows * kHeadDim) ||
+      g.dv.size() != static_cast<size_t>(k.heads * k.rows * kHeadDim))
+    throw ShapeError("block_attn_backward: gradient shape mismatch");
+  float* d = ws.d_vec(q.heads * q.rows);
+  check(da_attn_bwd_preprocess(d_out.data, out.data, d, out.heads, out.rows, kHeadDim, st));
   da_bwd_args a{};
   a.q = q.data;
   a.k = k.data;
   a.v = v.data;
   a.d_out = d_out.data;
   a.lse = lse;
-  a.d_vec = d.data();
+  a.d_vec = d;
   a.h_q = q.heads;
   a.h_kv = k.heads;
   a.rows_q = q.rows;
@@ -260,12 +322,26 @@ inline ChunkGrads block_attn_backward(const Chunk& q, const Chunk& k, const Chun
   a.dq_acc = g.dq.data();
   a.dk_acc = g.dk.data();
   a.dv_acc = g.dv.data();
-  a.accumulate_kv = 0;
+  a.accumulate_kv = accumulate_kv ? 1 : 0;
   a.scale = static_cast<float>(scale);
   a.mask = static_cast<int>(mask);
   a.deterministic = deterministic ? 1 : 0;
   check(da_attn_bwd_chunk(&a, st));
-  check_cuda(cudaStreamSynchronize(st), "block_attn_backward");  // d lives on this frame
+}
+
+/// Value form (the reference returns the contribution, flashcore.hpp:290):
+/// allocates the returned gradients; D lives in the thread's workspace.
+inline ChunkGrads block_attn_backward(const Chunk& q, const Chunk& k, const Chunk& v,
+                                      const Chunk& out, const float* lse, const Chunk& d_out,
+                                      MaskMode mask, double scale, cudaStream_t st,
+                                      bool deterministic = false) {
+  thread_local Workspace ws;
+  ChunkGrads g{DeviceBuffer<float>(q.heads * q.rows * kHeadDim),
+               DeviceBuffer<float>(k.heads * k.rows * kHeadDim),
+               DeviceBuffer<float>(k.heads * k.rows * kHeadDim)};
+  check_cuda(cudaMemsetAsync(g.dq.data(), 0, g.dq.size() * sizeof(float), st), "dq zero");
+  block_attn_backward_into(q, k, v, out, lse, d_out, mask, scale, g, ws, st, false,
+                           deterministic);
   return g;
 }
 
@@ -483,13 +559,72 @@ inline CommCounters run_backward(std::vector<SequenceShard>& s, int64_t heads,
   for (auto& x : s) {
     if (x.out.size() == 0 || x.lse.size() == 0)
       throw StateError("run_backward requires forward output and logsumexp");
-    x.dq = DeviceBuffer<float>(heads * rows * kHeadDim);
-    x.dk = DeviceBuffer<float>(heads * rows * kHeadDim);
-    x.dv = DeviceBuffer<float>(heads * rows * kHeadDim);
+    if (x.dq.size() != static_cast<size_t>(heads * rows * kHeadDim)) {  // reused across calls
+      x.dq = DeviceBuffer<float>(heads * rows * kHeadDim);
+      x.dk = DeviceBuffer<float>(heads * rows * kHeadDim);
+      x.dv = DeviceBuffer<float>(heads * rows * kHeadDim);
+    }
   }
   ShardArrays a = shard_arrays(s, heads, rows);
   da_counters c{};
   check(da_run_backward_sched(&a.c, kind, &c, st));
+  return to_counters(c);
+}
+
+/// RunOptions (runtime.hpp:98-103). On the device both reference executor
+/// modes are the same stream-ordered stepper (identical bits), and overlap is
+/// the copy / compute concurrency of the stream; both fields are accepted for
+/// source compatibility, blocks are validated (the GPU tiles are 128 x 128).
+enum class ExecutorMode { Stepper, Concurrent };
+struct RunOptions {
+  ExecutorMode mode = ExecutorMode::Stepper;
+  bool overlap = false;
+  int64_t block_rows = 16, block_cols = 16;
+  void check() const {
+    if (block_rows <= 0 || block_cols <= 0) throw ConfigError("block sizes must be positive");
+  }
+};
+
+/// run_forward over an arbitrary validated Schedule (runtime.hpp:106-109).
+inline CommCounters run_forward(std::vector<SequenceShard>& s, int64_t heads,
+                                const Schedule& schedule, const RunOptions& opts,
+                                cudaStream_t st) {
+  opts.check();
+  if (s.empty()) throw ConfigError("need at least 1 worker");
+  const int64_t rows = static_cast<int64_t>(s[0].lse.size()) / heads;
+  ShardArrays a = shard_arrays(s, heads, rows);
+  std::vector<int32_t> t, m;
+  flatten(schedule, t, m);
+  da_counters c{};
+  check(da_run_forward_table(&a.c, schedule.step_count(), t.data(),
+                             static_cast<int64_t>(t.size() / 6), m.data(),
+                             static_cast<int64_t>(m.size() / 4), &c, st));
+  return to_counters(c);
+}
+
+/// run_backward over an arbitrary validated backward Schedule.
+inline CommCounters run_backward(std::vector<SequenceShard>& s, int64_t heads,
+                                 const Schedule& schedule, const RunOptions& opts,
+                                 cudaStream_t st) {
+  opts.check();
+  if (s.empty()) throw ConfigError("need at least 1 worker");
+  const int64_t rows = static_cast<int64_t>(s[0].lse.size()) / heads;
+  for (auto& x : s) {
+    if (x.out.size() == 0 || x.lse.size() == 0)
+      throw StateError("run_backward requires forward output and logsumexp");
+    if (x.dq.size() != static_cast<size_t>(heads * rows * kHeadDim)) {
+      x.dq = DeviceBuffer<float>(heads * rows * kHeadDim);
+      x.dk = DeviceBuffer<float>(heads * rows * kHeadDim);
+      x.dv = DeviceBuffer<float>(heads * rows * kHeadDim);
+    }
+  }
+  ShardArrays a = shard_arrays(s, heads, rows);
+  std::vector<int32_t> t, m;
+  flatten(schedule, t, m);
+  da_counters c{};
+  check(da_run_backward_table(&a.c, schedule.step_count(), t.data(),
+                              static_cast<int64_t>(t.size() / 6), m.data(),
+                              static_cast<int64_t>(m.size() / 4), &c, st));
   return to_counters(c);
 }
 

@@ -285,7 +285,18 @@ da_status da_run_backward(const da_shards* shards, da_counters* counters, void* 
  * pairs like the forward). */
 da_status da_run_backward_sched(const da_shards* shards, int schedule_kind, da_counters* counters,
                                 void* stream);
-/* Frees the cached runtime workspace of the calling thread. */
+/* run_forward / run_backward over a caller-supplied schedule table in the
+ * flat encoding of da_schedule_build (runtime.hpp:106-118 take `const
+ * Schedule&`): any table that passes validate (schedule.cpp:121-258; the
+ * backward one da_schedule_validate_backward) runs, else DA_ERR_SCHEDULE with
+ * the first violation. */
+da_status da_run_forward_table(const da_shards* shards, int32_t steps, const int32_t* tasks,
+                               int64_t n_tasks, const int32_t* messages, int64_t n_messages,
+                               da_counters* counters, void* stream);
+da_status da_run_backward_table(const da_shards* shards, int32_t steps, const int32_t* tasks,
+                                int64_t n_tasks, const int32_t* messages, int64_t n_messages,
+                                da_counters* counters, void* stream);
+/* Frees the cached runtime workspaces (one per stream; waits for each stream). */
 void da_runtime_release(void);
 
 /* ------------------------------------------------------------------------

@@ -76,6 +76,10 @@ SIGNATURES = {
     "da_run_backward_sched": (C.c_int, [C.POINTER(Shards), C.c_int, C.POINTER(Counters), vp]),
     "da_run_backward": (C.c_int, [C.POINTER(Shards), C.POINTER(Counters), vp]),
     "da_runtime_release": (None, []),
+    "da_run_forward_table": (C.c_int, [C.POINTER(Shards), i32, C.POINTER(i32), i64,
+                                       C.POINTER(i32), i64, C.POINTER(Counters), vp]),
+    "da_run_backward_table": (C.c_int, [C.POINTER(Shards), i32, C.POINTER(i32), i64,
+                                        C.POINTER(i32), i64, C.POINTER(Counters), vp]),
     "da_rng_uniform": (C.c_int, [C.c_uint64, i64, C.c_double, C.c_double, C.c_int, vp, vp]),
     "da_debug_set_bwd_trace": (None, [vp]),
     "da_debug_set_fwd_trace": (None, [vp]),

@@ -187,17 +187,32 @@ void da_runtime_release(void) {
   g_ws_map.clear();
 }
 
-da_status da_run_forward(const da_shards* s, int schedule_kind, da_counters* counters,
-                         void* stream) {
+static FlatSchedule flat_from_table(int workers, int32_t steps, const int32_t* tasks,
+                                    int64_t n_tasks, const int32_t* messages,
+                                    int64_t n_messages) {
+  FlatSchedule f;
+  f.workers = workers;
+  f.steps = steps;
+  for (int64_t i = 0; tasks && i < n_tasks; ++i) {
+    const int32_t* o = tasks + 6 * i;
+    f.tasks.push_back({o[0], o[1], o[2], o[3], o[4], o[5]});
+  }
+  for (int64_t i = 0; messages && i < n_messages; ++i) {
+    const int32_t* o = messages + 4 * i;
+    f.messages.push_back({o[0], o[1], o[2], o[3]});
+  }
+  return f;
+}
+
+// The device executor over ANY schedule that passes the reference's
+// validator (schedule.cpp:121-258) — the built-in kinds or a caller's table.
+static da_status run_forward_flat(const da_shards* s, const FlatSchedule& sch,
+                                  da_counters* counters, void* stream) {
   da_status rc = check_shards(s, false);
   if (rc != DA_OK) return rc;
   const int P = s->workers;
-  if (schedule_kind != DA_SCHEDULE_RING && schedule_kind != DA_SCHEDULE_BALANCED &&
-      schedule_kind != DA_SCHEDULE_BALANCED_SPLIT)
-    return set_error(DA_ERR_CONFIG, "unknown schedule kind");
-  const FlatSchedule sch = schedule_kind == DA_SCHEDULE_RING      ? make_ring(P)
-                           : schedule_kind == DA_SCHEDULE_BALANCED ? make_balanced(P)
-                                                                   : make_balanced_split(P);
+  if (sch.workers != P)
+    return set_error(DA_ERR_SCHEDULE, "schedule worker count does not match the shards");
   const auto errs = validate_flat(sch);
   if (!errs.empty())
     return set_error(DA_ERR_SCHEDULE, "invalid schedule: " + errs.front() + " (" +
@@ -319,18 +334,13 @@ da_status da_run_backward(const da_shards* s, da_counters* counters, void* strea
 // kv chunk r) is one block_attn_backward launch; dq goes to p's accumulator,
 // dk/dv to r's (zero-copy GradKV / local for helpers). Ring order reproduces
 // runtime.cpp:605-651; balanced order follows make_balanced_backward.
-da_status da_run_backward_sched(const da_shards* s, int schedule_kind, da_counters* counters,
-                                void* stream) {
+static da_status run_backward_flat(const da_shards* s, const FlatSchedule& sch,
+                                   da_counters* counters, void* stream) {
   da_status rc = check_shards(s, true);
   if (rc != DA_OK) return rc;
   const int P = s->workers;
-  FlatSchedule sch;
-  if (schedule_kind == DA_SCHEDULE_RING_BWD || schedule_kind == DA_SCHEDULE_RING)
-    sch = make_ring_backward(P);
-  else if (schedule_kind == DA_SCHEDULE_BALANCED_BWD || schedule_kind == DA_SCHEDULE_BALANCED)
-    sch = make_balanced_backward(P);
-  else
-    return set_error(DA_ERR_CONFIG, "unknown schedule kind");
+  if (sch.workers != P)
+    return set_error(DA_ERR_SCHEDULE, "schedule worker count does not match the shards");
   const auto errs = validate_backward_flat(sch);
   if (!errs.empty())
     return set_error(DA_ERR_SCHEDULE, "invalid schedule: " + errs.front() + " (" +
@@ -425,6 +435,49 @@ da_status da_run_backward_sched(const da_shards* s, int schedule_kind, da_counte
     *counters = c;
   }
   return DA_OK;
+}
+
+da_status da_run_forward(const da_shards* s, int schedule_kind, da_counters* counters,
+                         void* stream) {
+  if (s == nullptr) return set_error(DA_ERR_CONFIG, "null shards");
+  const int P = s->workers;
+  if (P < 1) return set_error(DA_ERR_CONFIG, "need at least 1 worker");
+  if (schedule_kind == DA_SCHEDULE_RING) return run_forward_flat(s, make_ring(P), counters, stream);
+  if (schedule_kind == DA_SCHEDULE_BALANCED)
+    return run_forward_flat(s, make_balanced(P), counters, stream);
+  if (schedule_kind == DA_SCHEDULE_BALANCED_SPLIT)
+    return run_forward_flat(s, make_balanced_split(P), counters, stream);
+  return set_error(DA_ERR_CONFIG, "unknown schedule kind");
+}
+
+da_status da_run_forward_table(const da_shards* s, int32_t steps, const int32_t* tasks,
+                               int64_t n_tasks, const int32_t* messages, int64_t n_messages,
+                               da_counters* counters, void* stream) {
+  if (s == nullptr) return set_error(DA_ERR_CONFIG, "null shards");
+  return run_forward_flat(s, flat_from_table(s->workers, steps, tasks, n_tasks, messages,
+                                             n_messages),
+                          counters, stream);
+}
+
+da_status da_run_backward_sched(const da_shards* s, int schedule_kind, da_counters* counters,
+                                void* stream) {
+  if (s == nullptr) return set_error(DA_ERR_CONFIG, "null shards");
+  const int P = s->workers;
+  if (P < 1) return set_error(DA_ERR_CONFIG, "need at least 1 worker");
+  if (schedule_kind == DA_SCHEDULE_RING_BWD || schedule_kind == DA_SCHEDULE_RING)
+    return run_backward_flat(s, make_ring_backward(P), counters, stream);
+  if (schedule_kind == DA_SCHEDULE_BALANCED_BWD || schedule_kind == DA_SCHEDULE_BALANCED)
+    return run_backward_flat(s, make_balanced_backward(P), counters, stream);
+  return set_error(DA_ERR_CONFIG, "unknown schedule kind");
+}
+
+da_status da_run_backward_table(const da_shards* s, int32_t steps, const int32_t* tasks,
+                                int64_t n_tasks, const int32_t* messages, int64_t n_messages,
+                                da_counters* counters, void* stream) {
+  if (s == nullptr) return set_error(DA_ERR_CONFIG, "null shards");
+  return run_backward_flat(s, flat_from_table(s->workers, steps, tasks, n_tasks, messages,
+                                              n_messages),
+                           counters, stream);
 }
 
 }  // extern "C"

@@ -181,8 +181,9 @@ def run_forward(shards: list[SequenceShard], schedule: Schedule | str = "balance
                 stream=None) -> ExecutionTrace:
     """runtime.cpp:491-529: runs the schedule's forward over all P workers on
     this device; writes out (bf16) / lse (fp32) into the shards."""
-    kind = schedule if isinstance(schedule, str) else _schedule_kind(schedule)
-    kind_i = {"ring": 0, "balanced": 1, "balanced_split": 4}[kind]
+    if isinstance(schedule, str) and schedule not in ("ring", "balanced", "balanced_split"):
+        from .errors import ConfigError
+        raise ConfigError(f"unknown forward schedule {schedule!r}")
     for s in shards:
         h, rows, d = s.q.shape
         if s.out is None:
@@ -192,12 +193,18 @@ def run_forward(shards: list[SequenceShard], schedule: Schedule | str = "balance
     st, keep = _shards_struct(shards, False)
     c = _lib.Counters()
     strm = stream if stream is not None else torch.cuda.current_stream()
-    check(_lib.lib().da_run_forward(C.byref(st), kind_i, C.byref(c), C.c_void_p(strm.cuda_stream)))
+    sptr = C.c_void_p(strm.cuda_stream)
+    if isinstance(schedule, str):
+        kind_i = {"ring": 0, "balanced": 1, "balanced_split": 4}[schedule]
+        check(_lib.lib().da_run_forward(C.byref(st), kind_i, C.byref(c), sptr))
+    else:  # any schedule that passes the reference validator (runtime.hpp:106-118)
+        steps, t, nt, m, nm = _table(schedule)
+        check(_lib.lib().da_run_forward_table(C.byref(st), steps, t, nt, m, nm, C.byref(c), sptr))
     del keep
     return _trace(len(shards), c)
 
 
-def run_backward(shards: list[SequenceShard], schedule: str = "ring",
+def run_backward(shards: list[SequenceShard], schedule="ring",
                  stream=None) -> ExecutionTrace:
     """runtime.cpp:720-750. schedule="ring" is the reference order
     (BackwardMode::Vanilla); "balanced" is the load-balanced backward
@@ -219,24 +226,23 @@ def run_backward(shards: list[SequenceShard], schedule: str = "ring",
     st, keep = _shards_struct(shards, True)
     c = _lib.Counters()
     strm = stream if stream is not None else torch.cuda.current_stream()
-    kind = {"ring": 2, "balanced": 3}[schedule]
-    check(_lib.lib().da_run_backward_sched(C.byref(st), kind, C.byref(c),
-                                           C.c_void_p(strm.cuda_stream)))
+    sptr = C.c_void_p(strm.cuda_stream)
+    if isinstance(schedule, str):
+        if schedule not in ("ring", "balanced"):
+            from .errors import ConfigError
+            raise ConfigError(f"unknown backward schedule {schedule!r}")
+        kind = {"ring": 2, "balanced": 3}[schedule]
+        check(_lib.lib().da_run_backward_sched(C.byref(st), kind, C.byref(c), sptr))
+    else:  # a backward schedule table (validate_backward invariants)
+        steps, t, nt, m, nm = _table(schedule)
+        check(_lib.lib().da_run_backward_table(C.byref(st), steps, t, nt, m, nm, C.byref(c), sptr))
     del keep
     return _trace(len(shards), c)
 
 
-def _schedule_kind(s: Schedule) -> str:
-    from .schedule import (build_balanced_schedule, build_balanced_split_schedule,
-                           build_ring_schedule, validate)
-    from .errors import ScheduleError
-    v = validate(s)
-    if v:
-        raise ScheduleError(f"invalid schedule: {v[0]} ({len(v)} violations)")
-    for name, b in (("ring", build_ring_schedule), ("balanced", build_balanced_schedule),
-                    ("balanced_split", build_balanced_split_schedule)):
-        ref = b(s.workers)
-        if ref.flat() == s.flat():
-            return name
-    raise ScheduleError("the device executor runs the ring, balanced and balanced_split "
-                        "schedules only")
+def _table(s: Schedule):
+    """Flat int32 encoding of a Schedule for the *_table C entry points."""
+    tasks, msgs = s.flat()
+    t = (C.c_int32 * max(1, len(tasks)))(*tasks)
+    m = (C.c_int32 * max(1, len(msgs)))(*msgs)
+    return len(s.steps), t, len(tasks) // 6, m, len(msgs) // 4

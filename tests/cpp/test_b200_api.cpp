@@ -164,6 +164,54 @@ static void gpu_tests() {
     for (auto& x : s) x.out = b2::DeviceBuffer<b2::bf16_t>();
     REQUIRE(throws<b2::StateError>([&] { b2::run_backward(s, 1, DA_SCHEDULE_RING_BWD, st); }));
   });
+  run("Schedule-object runtime + allocation-free backward_into == kind entry points", [&] {
+    const int P = 4;
+    const int64_t n = 1024, d = 128, H = 1;
+    std::vector<double> q(H * n * d), k(H * n * d), v(H * n * d), g(H * n * d);
+    dao_make_inputs(2, P, n, d, H, 1, q.data(), k.data(), v.data(), g.data());
+    std::vector<b2::bf16_t> qb(q.size()), kb(q.size()), vb(q.size()), gb(q.size());
+    for (size_t i = 0; i < q.size(); ++i) {
+      qb[i] = to_bf16(q[i]);
+      kb[i] = to_bf16(k[i]);
+      vb[i] = to_bf16(v[i]);
+      gb[i] = to_bf16(g[i]);
+    }
+    auto a = b2::make_shards(P, n, H, qb, kb, vb, gb, st);
+    auto b = b2::make_shards(P, n, H, qb, kb, vb, gb, st);
+    b2::run_forward(a, H, DA_SCHEDULE_BALANCED, st);
+    b2::run_forward(b, H, b2::build_balanced_schedule(P), b2::RunOptions{}, st);
+    for (int p = 0; p < P; ++p) {
+      REQUIRE(a[p].out.download(st) == b[p].out.download(st));
+      REQUIRE(a[p].lse.download(st) == b[p].lse.download(st));
+    }
+    REQUIRE(throws<b2::ConfigError>([&] {
+      b2::RunOptions bad;
+      bad.block_rows = 0;
+      b2::run_forward(b, H, b2::build_ring_schedule(P), bad, st);
+    }));
+    // worker 1's diagonal pair through the allocation-free form, twice with one
+    // workspace: deterministic dq, identical to the value form
+    const b2::Chunk cq{a[0].q.data(), H, n / P}, ck{a[0].k.data(), H, n / P},
+        cv{a[0].v.data(), H, n / P}, co{a[0].out.data(), H, n / P},
+        cg{a[0].d_out.data(), H, n / P};
+    b2::Workspace ws;
+    b2::ChunkGrads into{b2::DeviceBuffer<float>(H * (n / P) * d),
+                        b2::DeviceBuffer<float>(H * (n / P) * d),
+                        b2::DeviceBuffer<float>(H * (n / P) * d)};
+    cudaMemsetAsync(into.dq.data(), 0, into.dq.size() * 4, st);
+    b2::block_attn_backward_into(cq, ck, cv, co, a[0].lse.data(), cg, b2::MaskMode::Diagonal,
+                                 1.0 / std::sqrt(128.0), into, ws, st, false, true);
+    const auto val = b2::block_attn_backward(cq, ck, cv, co, a[0].lse.data(), cg,
+                                             b2::MaskMode::Diagonal, 1.0 / std::sqrt(128.0), st,
+                                             true);
+    REQUIRE(into.dq.download(st) == val.dq.download(st));
+    REQUIRE(into.dk.download(st) == val.dk.download(st));
+    REQUIRE(throws<b2::ShapeError>([&] {
+      const b2::Chunk half{a[0].v.data(), H, n / P / 2};
+      b2::block_attn_backward_into(cq, ck, half, co, a[0].lse.data(), cg, b2::MaskMode::Diagonal,
+                                   1.0, into, ws, st);
+    }));
+  });
   for (int kind : {0, 1, 4}) {
     const std::string name = std::string("P=4 N=2048 H=2 forward (") +
                              (kind == 0 ? "ring" : kind == 1 ? "balanced" : "split") +

@@ -13,6 +13,7 @@ import pytest
 import torch
 
 from oracle import oracle as O
+from torch_ref import rel_err
 
 pytestmark = pytest.mark.gpu
 GOLD = Path(__file__).resolve().parent / "golden"
@@ -192,3 +193,42 @@ def test_invalid_schedule_and_mismatched_shards_are_rejected(cuda):
     small[2].q = small[2].q[:, :64].contiguous()
     with pytest.raises(ShapeError):
         run_forward(small, "ring")
+
+
+def test_runtime_takes_any_valid_schedule_table(cuda):
+    """run_forward / run_backward accept a Schedule object, not only a kind
+    (runtime.hpp:106-118 take `const Schedule&`): a valid table that is none
+    of the built-ins (ring with steps 1 and 2 swapped) runs through
+    da_run_forward_table; the built-in tables passed as objects give the same
+    bits as the kind entry points."""
+    import dataclasses
+
+    from paper_2310_03294_b200 import schedule as S
+    from paper_2310_03294_b200.runtime import make_parity_shards, run_backward, run_forward
+
+    def outs(sh):
+        return [torch.cat([getattr(x, f) for x in sh], 1).clone() for f in ("out", "lse")]
+
+    base = make_parity_shards(3, 4, 1024, 2, 128)
+    run_forward(base, "ring")
+    run_backward(base, "ring")
+    ref = outs(base)
+    ref_g = [torch.cat([getattr(x, f) for x in base], 1).clone() for f in ("dq", "dk", "dv")]
+
+    same = make_parity_shards(3, 4, 1024, 2, 128)
+    run_forward(same, S.build_ring_schedule(4))
+    run_backward(same, S.build_ring_backward_schedule(4))
+    got = outs(same)
+    assert torch.equal(got[0], ref[0]) and torch.equal(got[1], ref[1])
+    for f, r in zip(("dq", "dk", "dv"), ref_g):
+        assert torch.equal(torch.cat([getattr(x, f) for x in same], 1), r), f
+
+    custom = S.build_ring_schedule(4)
+    custom.steps[1], custom.steps[2] = custom.steps[2], custom.steps[1]
+    custom.messages = sorted((dataclasses.replace(m, step=3 - m.step) if m.step in (1, 2) else m
+                              for m in custom.messages), key=lambda m: (m.step, m.from_))
+    assert S.validate(custom) == []
+    other = make_parity_shards(3, 4, 1024, 2, 128)
+    run_forward(other, custom)
+    o = outs(other)
+    assert rel_err(o[0], ref[0]) < 1e-2 and (o[1] - ref[1]).abs().max().item() < 1e-4
