@@ -629,13 +629,21 @@ inline CommCounters run_backward(std::vector<SequenceShard>& s, int64_t heads,
 }
 
 /// One rank of the sequence-parallel runtime, one process per GPU
-/// (runtime.cpp:390-487, 653-716 for a single worker): messages are
-/// copy-engine pulls from the peers' HBM. `allgather` bootstraps the IPC
-/// mappings (e.g. MPI_Allgather or torch.distributed); calls are collective.
+/// (runtime.cpp:390-487, 653-716 for a single worker): messages go over
+/// NCCL send/recv or copy-engine pulls from the peers' HBM. `allgather`
+/// bootstraps the IPC mappings / the NCCL id (e.g. MPI_Allgather or
+/// torch.distributed); calls are collective.
 class RankRuntime {
  public:
   RankRuntime(int rank, int world, da_allgather_fn allgather, void* ctx) {
     check(da_rank_create(rank, world, allgather, ctx, &h_));
+  }
+  /// opts.transport: DA_TRANSPORT_NCCL (send/recv per phase on a side stream),
+  /// DA_TRANSPORT_IPC (copy-engine pulls) or DA_TRANSPORT_NONE (no-comm arm);
+  /// opts.deterministic: bitwise-reproducible backward.
+  RankRuntime(int rank, int world, da_allgather_fn allgather, void* ctx,
+              const da_rank_options& opts) {
+    check(da_rank_create_ex(rank, world, allgather, ctx, &opts, &h_));
   }
   ~RankRuntime() { da_rank_destroy(h_); }
   RankRuntime(const RankRuntime&) = delete;

@@ -300,32 +300,63 @@ da_status da_run_backward_table(const da_shards* shards, int32_t steps, const in
 void da_runtime_release(void);
 
 /* ------------------------------------------------------------------------
- * Per-rank runtime: one process (or thread) per GPU, each holding ONE
- * contiguous chunk of the sequence — the reference's worker (runtime.cpp:
- * 390-487 concurrent executor, 653-716 backward) with every message a
- * copy-engine pull from the peer's HBM (CUDA IPC, over NVLink between GPUs)
- * ordered by device-side counters (da_stream_write_u32 / wait). No NCCL.
+ * Per-rank runtime: one process per GPU, each holding ONE contiguous chunk
+ * of the sequence — the reference's worker (runtime.cpp:390-487 concurrent
+ * executor, 653-716 backward). A pass is a fixed sequence of phases,
+ * identical on every rank: operands(0), then per step t operands(t+1)
+ * (prefetch depth 1, runtime.cpp:280-284) and results(t) (partials,
+ * GradKV, dq partials), all on a high-priority side stream. Transports:
+ *   DA_TRANSPORT_NCCL  one ncclGroupStart/Send/Recv/GroupEnd per phase
+ *                      (NCCL is dlopen'ed: libnccl.so.2);
+ *   DA_TRANSPORT_IPC   copy-engine pulls from the peer's HBM (CUDA IPC)
+ *                      ordered by device counters (da_stream_write_u32 /
+ *                      wait); ranks may share one GPU;
+ *   DA_TRANSPORT_NONE  no transfer: receive slots are filled once from the
+ *                      rank's own buffers — the same kernels on local data,
+ *                      the no-communication timing arm (analyzer.cpp:60-64).
+ * deterministic != 0 orders every dq reduction (bitwise reproducible
+ * backward; the reference's executors are, runtime.hpp:7-9).
  *
- * Bootstrap and per-pass publication of the pulled buffers go through the
- * caller's allgather (e.g. torch.distributed, MPI): `fn(ctx, send, bytes,
- * recv)` must gather `bytes` from every rank into recv[world * bytes] in rank
- * order and return 0. All da_rank_* calls are collective over the ranks.
- * Forward: q [h_q, rows, 128], k/v [h_kv, rows, 128] bf16 of this rank;
- * writes out (bf16) and lse (fp32) and keeps them (the rematerialisation
- * state) for da_rank_backward, which writes fp32 dq [h_q], dk/dv [h_kv].
- * schedule_kind: DA_SCHEDULE_RING / BALANCED / BALANCED_SPLIT (forward),
- * DA_SCHEDULE_RING_BWD / BALANCED_BWD (backward).
+ * Bootstrap (IPC handles, the NCCL unique id) and per-pass IPC publication
+ * go through the caller's allgather (e.g. torch.distributed, MPI):
+ * `fn(ctx, send, bytes, recv)` must gather `bytes` from every rank into
+ * recv[world * bytes] in rank order and return 0. All da_rank_* calls are
+ * collective over the ranks. Forward: q [h_q, rows, 128], k/v [h_kv, rows,
+ * 128] bf16 of this rank; writes out (bf16) and lse (fp32) and keeps them (the
+ * rematerialisation state) for da_rank_backward, which writes fp32 dq [h_q],
+ * dk/dv [h_kv]. schedule_kind: DA_SCHEDULE_RING / BALANCED / BALANCED_SPLIT
+ * (forward), DA_SCHEDULE_RING_BWD / BALANCED_BWD (backward).
  * ------------------------------------------------------------------------ */
 typedef int (*da_allgather_fn)(void* ctx, const void* send, uint64_t bytes, void* recv);
 typedef struct da_rank da_rank;
 
+#define DA_TRANSPORT_IPC 0
+#define DA_TRANSPORT_NCCL 1
+#define DA_TRANSPORT_NONE 2
+
+typedef struct da_rank_options {
+  int transport;     /* DA_TRANSPORT_* */
+  int deterministic; /* ordered dq reductions in every backward chunk */
+  int nccl_max_ctas; /* > 0: cap the CTAs of NCCL's kernels (SMs left to attention) */
+} da_rank_options;
+
+/* da_rank_create = da_rank_create_ex with {DA_TRANSPORT_IPC, 0, 0}. */
 da_status da_rank_create(int rank, int world, da_allgather_fn fn, void* ctx, da_rank** out);
+da_status da_rank_create_ex(int rank, int world, da_allgather_fn fn, void* ctx,
+                            const da_rank_options* opts, da_rank** out);
 void da_rank_destroy(da_rank* r);
 da_status da_rank_forward(da_rank* r, int schedule_kind, const void* q, const void* k,
                           const void* v, int64_t h_q, int64_t h_kv, int64_t rows, void* out,
                           float* lse, da_counters* counters, void* stream);
 da_status da_rank_backward(da_rank* r, int schedule_kind, const void* d_out, float* dq, float* dk,
                            float* dv, da_counters* counters, void* stream);
+/* The message protocol of one rank without a device: 5 int32 per entry
+ * {pass (0 forward, 1 backward), phase (2t = operands(t), 2t+1 = results(t)),
+ * dir (0 send, 1 receive), peer rank, buffer key}; *n = entries (written up to
+ * cap; out may be NULL to count). Every send must meet exactly one receive
+ * of the same key in the same phase (checked by tests/test_rank_protocol.py). */
+da_status da_rank_protocol(int world, int rank, int fwd_kind, int bwd_kind, int32_t* out,
+                           int64_t cap, int64_t* n);
 
 
 /* Device fill with the reference's splitmix64 stream (numerics.hpp:140-174):

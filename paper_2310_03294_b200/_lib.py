@@ -38,6 +38,13 @@ class Shards(C.Structure):
                 ("dq", C.POINTER(vp)), ("dk", C.POINTER(vp)), ("dv", C.POINTER(vp))]
 
 
+class RankOptions(C.Structure):
+    _fields_ = [("transport", C.c_int), ("deterministic", C.c_int), ("nccl_max_ctas", C.c_int)]
+
+
+TRANSPORT = {"ipc": 0, "nccl": 1, "none": 2}
+
+
 class Counters(C.Structure):
     _fields_ = [("kv_scalars", i64), ("q_scalars", i64), ("partial_scalars", i64),
                 ("grad_scalars", i64), ("kv_messages", i64), ("q_messages", i64),
@@ -56,6 +63,9 @@ SIGNATURES = {
     "da_stream_write_u32": (C.c_int, [vp, vp, C.c_uint32]),
     "da_rank_create": (C.c_int, [C.c_int, C.c_int, vp, vp, C.POINTER(vp)]),
     "da_rank_destroy": (None, [vp]),
+    "da_rank_create_ex": (C.c_int, [C.c_int, C.c_int, vp, vp, vp, C.POINTER(vp)]),
+    "da_rank_protocol": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(i32), i64,
+                                   C.POINTER(i64)]),
     "da_rank_forward": (C.c_int, [vp, C.c_int, vp, vp, vp, i64, i64, i64, vp, vp, vp, vp]),
     "da_rank_backward": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, vp, vp]),
     "da_stream_wait_u32_geq": (C.c_int, [vp, vp, C.c_uint32]),

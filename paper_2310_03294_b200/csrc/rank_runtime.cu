@@ -3,32 +3,47 @@
 // Each rank holds ONE contiguous chunk and runs the reference worker's
 // operation order (runtime.cpp:390-487 forward, 653-716 backward; per step:
 // the primary task, then the merges in helper order) from the same flat
-// schedule tables as the rest of the library (schedule.cpp). Messages are
-// pulls: the receiver's side stream copies straight from the sender's HBM
-// (CUDA IPC mapping; the copy engines move the bytes over NVLink, no SM and
-// no NCCL kernel involved) into its receive slot, prefetched one step ahead
-// (double-buffered slots: the reference's residency bound of 2).
+// schedule tables as the rest of the library (schedule.cpp).
 //
-// Ordering between ranks uses 32-bit counters in device memory (csrc/peer.cu):
-//   flags[dst]          "ready": bumped on the sender's compute stream after
-//                       the producer of the n-th message to dst
-//   flags[world + src]  "done": bumped on the receiver's side stream after
-//                       the n-th pull from src
-// The receiver's side stream waits for ready >= n before pulling; a sender
-// that reuses a buffer (partials, gradient slots) or returns to its caller
-// first waits (in its stream) for done >= n. Messages of a pair are matched
-// by order, exactly as both sides walk the same schedule.
+// Protocol. A pass is a fixed sequence of PHASES, identical on every rank:
+//   operands(0), operands(1), results(0), operands(2), results(1), ...
+// operands(t) carries the messages step t consumes (KV / KVHalf / Q, and for
+// the backward the (q, dO, lse, D) bundle), posted one step ahead (prefetch
+// depth 1 into double-buffered slots: the reference's residency bound of 2,
+// runtime.cpp:280-284, 427-431); results(t) carries what step t produces
+// (Partial, GradKV, dq partials), right after its kernels. The phase lists
+// are built by one pure function (program()) from the schedule, so sender
+// and receiver derive every message from the same table; da_rank_protocol()
+// exposes them and the CPU tests check that every send has exactly one
+// matching receive in the same phase, in the same order.
 //
-// Publication: before a pass every rank allgathers, per pulled buffer, the
-// IPC handle of its allocation and the offset inside it (through the
-// caller's allgather); peers open each allocation once and cache it.
+// Transports, chosen at creation (da_rank_options.transport):
+//   NCCL  each phase is one ncclGroupStart/Send/Recv/GroupEnd on a
+//         high-priority side stream, after an event from the compute stream
+//         (north_star: K/V prefetched with NCCL send/recv over NVLink on a
+//         side stream). Identical phase order on all ranks makes the groups
+//         deadlock-free. NCCL is dlopen'ed (libnccl.so.2 — in a torch
+//         process the already-loaded copy), so the library loads without it.
+//   IPC   the receiver's side stream pulls straight from the sender's HBM
+//         (CUDA IPC mapping; copy engines, no SM), ordered by 32-bit device
+//         counters (csrc/peer.cu): flags[dst] "ready" bumped on the sender's
+//         compute stream after the producer of the n-th message to dst;
+//         flags[world + src] "done" bumped on the receiver's side stream
+//         after the n-th pull from src. Works for ranks that share one GPU.
+//   NONE  no transfer: every receive slot is filled ONCE from the rank's own
+//         buffer of the same kind and then reused, so the same kernels run on
+//         local data — the no-communication arm that exposed communication is
+//         measured against (analyzer.cpp:60-64). Results are not attention.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <array>
 #include <cstring>
 #include <map>
 #include <memory>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -42,17 +57,152 @@ extern "C" da_status da_stream_wait_u32_geq(void* stream, const void* addr, uint
 namespace da {
 namespace {
 
-// buffers peers pull from (per pass)
+// buffers a rank sends (per pass)
 enum Key : int {
   kK = 0, kV, kQ, kPart, kKHi, kVHi,                    // forward
   kDOut, kLse, kDVec, kGK0, kGV0, kGK1, kGV1, kGQ0, kGQ1,  // backward
   kNumKeys
 };
 
+// receive slots (resolved to device addresses by the executor)
+enum Slot : int { kSlotKV = 0, kSlotKVH, kSlotQ, kSlotPart, kSlotBundle, kSlotGrad, kSlotGQ };
+
+struct XSend {
+  int dst;  // 0-based rank
+  Key key;
+};
+struct XRecv {
+  int src;  // 0-based rank
+  Key key;
+  Slot slot;
+  int index;  // slot parity (t % 2) or the helper's worker id for partials
+  int part;   // byte offset selector inside a multi-tensor slot (0..3)
+};
+struct Phase {
+  std::vector<XSend> sends;
+  std::vector<XRecv> recvs;
+  bool empty() const { return sends.empty() && recvs.empty(); }
+};
+
+struct Plan {
+  int action = 0;  // 0 idle, 1 local, 2 direct, 3 help
+  int peer = 0;    // 1-based
+  int part = kPartWhole;
+  std::vector<int> kv_sends, kvh_sends, q_sends, merges, gradkv_from, gradkv_to;
+};
+
+std::vector<Plan> plans_for(const FlatSchedule& s, int worker) {
+  std::vector<Plan> plans(s.steps);
+  for (const Task& k : s.tasks) {
+    if (k.worker != worker) continue;
+    Plan& p = plans[k.step];
+    if (k.kind == kLocal) {
+      p.action = 1;
+    } else if (k.kind == kRemote) {
+      p.action = k.query_owner == worker ? 2 : 3;
+      p.peer = k.query_owner == worker ? k.kv_owner : k.query_owner;
+      p.part = k.helper;
+    } else if (k.kind == kMerge) {
+      p.merges.push_back(k.helper);
+    }
+  }
+  for (const Message& m : s.messages) {
+    Plan& p = plans[m.step];
+    if (m.from == worker && m.kind == kMsgKV) p.kv_sends.push_back(m.to);
+    if (m.from == worker && m.kind == kMsgKVHalf) p.kvh_sends.push_back(m.to);
+    if (m.from == worker && m.kind == kMsgQ) p.q_sends.push_back(m.to);
+    if (m.to == worker && m.kind == kMsgGradKV) p.gradkv_from.push_back(m.from);
+    if (m.from == worker && m.kind == kMsgGradKV) p.gradkv_to.push_back(m.to);
+  }
+  return plans;
+}
+
+// The pass as phases: [operands(0)], then per step t: operands(t+1), results(t).
+struct Program {
+  std::vector<Plan> plans;
+  std::vector<Phase> operands;  // [t]
+  std::vector<Phase> results;   // [t]
+};
+
+da_status forward_program(const FlatSchedule& s, int worker, Program* out) {
+  Program pg;
+  pg.plans = plans_for(s, worker);
+  const int T = static_cast<int>(pg.plans.size());
+  pg.operands.resize(T);
+  pg.results.resize(T);
+  for (int t = 0; t < T; ++t) {
+    const Plan& p = pg.plans[t];
+    Phase& op = pg.operands[t];
+    for (int dst : p.kv_sends) op.sends.insert(op.sends.end(), {{dst - 1, kK}, {dst - 1, kV}});
+    for (int dst : p.kvh_sends)
+      op.sends.insert(op.sends.end(), {{dst - 1, kKHi}, {dst - 1, kVHi}});
+    for (int dst : p.q_sends) op.sends.push_back({dst - 1, kQ});
+    if (p.action == 2 && p.part == kPartHigh) {
+      op.recvs.push_back({p.peer - 1, kKHi, kSlotKVH, 0, 0});
+      op.recvs.push_back({p.peer - 1, kVHi, kSlotKVH, 0, 1});
+    } else if (p.action == 2) {
+      op.recvs.push_back({p.peer - 1, kK, kSlotKV, t % 2, 0});
+      op.recvs.push_back({p.peer - 1, kV, kSlotKV, t % 2, 1});
+    } else if (p.action == 3) {
+      op.recvs.push_back({p.peer - 1, kQ, kSlotQ, t % 2, 0});
+    }
+    Phase& res = pg.results[t];
+    if (p.action == 3) res.sends.push_back({p.peer - 1, kPart});
+    for (int hw : p.merges) res.recvs.push_back({hw - 1, kPart, kSlotPart, hw, 0});
+  }
+  *out = std::move(pg);
+  return DA_OK;
+}
+
+da_status backward_program(const FlatSchedule& s, int worker, Program* out) {
+  Program pg;
+  pg.plans = plans_for(s, worker);
+  const int T = static_cast<int>(pg.plans.size());
+  pg.operands.resize(T);
+  pg.results.resize(T);
+  for (int t = 0; t < T; ++t) {
+    const Plan& p = pg.plans[t];
+    // a direct pair's GradKV leaves with its task's results (the table's
+    // GradKV message must sit at that step and go to the kv owner)
+    const bool direct = p.action == 2;
+    if (p.gradkv_to.size() != (direct ? 1u : 0u) || (direct && p.gradkv_to[0] != p.peer))
+      return set_error(DA_ERR_SCHEDULE,
+                       "GradKV must leave at its direct task's step, to the kv owner");
+    if (p.gradkv_from.size() > 1)
+      return set_error(DA_ERR_SCHEDULE, "at most one GradKV per worker and step is supported");
+    Phase& op = pg.operands[t];
+    for (int dst : p.kv_sends) op.sends.insert(op.sends.end(), {{dst - 1, kK}, {dst - 1, kV}});
+    for (int dst : p.q_sends)
+      op.sends.insert(op.sends.end(),
+                      {{dst - 1, kQ}, {dst - 1, kDOut}, {dst - 1, kLse}, {dst - 1, kDVec}});
+    if (p.action == 2) {
+      op.recvs.push_back({p.peer - 1, kK, kSlotKV, t % 2, 0});
+      op.recvs.push_back({p.peer - 1, kV, kSlotKV, t % 2, 1});
+    } else if (p.action == 3) {
+      op.recvs.push_back({p.peer - 1, kQ, kSlotBundle, t % 2, 0});
+      op.recvs.push_back({p.peer - 1, kDOut, kSlotBundle, t % 2, 1});
+      op.recvs.push_back({p.peer - 1, kLse, kSlotBundle, t % 2, 2});
+      op.recvs.push_back({p.peer - 1, kDVec, kSlotBundle, t % 2, 3});
+    }
+    Phase& res = pg.results[t];
+    const Key gk = (t % 2) ? kGK1 : kGK0, gv = (t % 2) ? kGV1 : kGV0;
+    const Key gq = (t % 2) ? kGQ1 : kGQ0;
+    if (p.action == 2) res.sends.insert(res.sends.end(), {{p.peer - 1, gk}, {p.peer - 1, gv}});
+    if (p.action == 3) res.sends.push_back({p.peer - 1, gq});
+    for (int src : p.gradkv_from) {
+      res.recvs.push_back({src - 1, gk, kSlotGrad, 0, 0});
+      res.recvs.push_back({src - 1, gv, kSlotGrad, 0, 1});
+    }
+    for (int hw : p.merges) res.recvs.push_back({hw - 1, gq, kSlotGQ, hw, 0});
+  }
+  *out = std::move(pg);
+  return DA_OK;
+}
+
 struct PubRecord {
   cudaIpcMemHandle_t handle;
   uint64_t offset;
-  uint64_t base;   // sender-side allocation base (cache key together with the rank)
+  uint64_t base;
   int32_t valid;
   int32_t pad;
 };
@@ -77,26 +227,71 @@ struct Buf {
   T* as() const { return static_cast<T*>(p); }
 };
 
+// in-flight exchange: the compute stream waits on it before using received
+// data or rewriting a sent buffer
 struct Work {
-  cudaEvent_t done = nullptr;                 // pulls landed (side stream)
-  std::vector<std::pair<int, uint32_t>> expect;  // peers' done counters to await
+  cudaEvent_t done = nullptr;
+  std::vector<std::pair<int, uint32_t>> expect;  // IPC: peers' done counters to await
 };
+
+// NCCL entry points resolved at run time
+struct Nccl {
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*init_rank_config)(ncclComm_t*, int, ncclUniqueId, int, ncclConfig_t*) = nullptr;
+  ncclResult_t (*destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) =
+      nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+const Nccl& nccl() {
+  static Nccl n = [] {
+    Nccl x;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h == nullptr) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h == nullptr) return x;
+    auto sym = [&](const char* name) { return dlsym(h, name); };
+    x.get_unique_id = reinterpret_cast<decltype(x.get_unique_id)>(sym("ncclGetUniqueId"));
+    x.init_rank_config =
+        reinterpret_cast<decltype(x.init_rank_config)>(sym("ncclCommInitRankConfig"));
+    x.destroy = reinterpret_cast<decltype(x.destroy)>(sym("ncclCommDestroy"));
+    x.group_start = reinterpret_cast<decltype(x.group_start)>(sym("ncclGroupStart"));
+    x.group_end = reinterpret_cast<decltype(x.group_end)>(sym("ncclGroupEnd"));
+    x.send = reinterpret_cast<decltype(x.send)>(sym("ncclSend"));
+    x.recv = reinterpret_cast<decltype(x.recv)>(sym("ncclRecv"));
+    x.error_string = reinterpret_cast<decltype(x.error_string)>(sym("ncclGetErrorString"));
+    x.ok = x.get_unique_id && x.init_rank_config && x.destroy && x.group_start && x.group_end &&
+           x.send && x.recv && x.error_string;
+    return x;
+  }();
+  return n;
+}
 
 }  // namespace
 }  // namespace da
 
 struct da_rank {
   int rank = 0, world = 1;
+  da_rank_options opts{};
   da_allgather_fn ag = nullptr;
   void* ctx = nullptr;
   cudaStream_t side = nullptr;
+  // IPC
   int* flags = nullptr;                 // [2 * world]
   std::vector<int*> rflags;             // peers' flags (mapped)
   std::vector<uint32_t> sent, pulled;   // per peer
-  // (rank, allocation's IPC handle bytes) -> mapped base; the handle (not the
-  // address) keys the cache, so a reused address of a new allocation remaps
-  std::map<std::pair<int, std::string>, char*> opened;
+  std::map<std::pair<int, std::string>, char*> opened;   // (rank, IPC handle) -> mapped base
   std::vector<std::array<char*, da::kNumKeys>> remote;  // [rank][key]
+  // NCCL
+  ncclComm_t comm = nullptr;
+  // this pass's own buffers per key (sends; the NONE transport's slot fill)
+  std::array<const void*, da::kNumKeys> local{};
+  std::array<size_t, da::kNumKeys> key_bytes{};
+  std::set<void*> filled;  // NONE: receive slots already filled
   // forward state (the rematerialisation hook: saved O / LSE, never recomputed)
   const void *q = nullptr, *k = nullptr, *v = nullptr;
   void* out = nullptr;
@@ -116,14 +311,17 @@ da_status ck(cudaError_t e, const char* where) {
   return e == cudaSuccess ? DA_OK : cuda_error(e, where);
 }
 
+da_status nk(ncclResult_t e, const char* where) {
+  if (e == ncclSuccess) return DA_OK;
+  return set_error(DA_ERR_NCCL, std::string(where) + ": " + nccl().error_string(e));
+}
+
 #define DA_TRY(x)                    \
   do {                               \
     const da_status s_ = (x);        \
     if (s_ != DA_OK) return s_;      \
   } while (0)
 
-// cuMemGetAddressRange through the runtime's driver entry point (the library
-// must load without libcuda on machines that only build it)
 using AddrRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
 AddrRangeFn addr_range_fn() {
   static AddrRangeFn fn = [] {
@@ -138,22 +336,22 @@ AddrRangeFn addr_range_fn() {
   return fn;
 }
 
-// Publishes `ptrs` (nullptr = not published this pass) to every peer.
-da_status publish(da_rank* r, const std::array<const void*, kNumKeys>& ptrs) {
+// IPC: publishes this pass's sendable buffers (nullptr = none) to every peer.
+da_status publish(da_rank* r) {
   std::vector<PubRecord> mine(kNumKeys);
   for (int key = 0; key < kNumKeys; ++key) {
     PubRecord& rec = mine[key];
     std::memset(&rec, 0, sizeof(rec));
-    if (ptrs[key] == nullptr) continue;
+    if (r->local[key] == nullptr) continue;
     CUdeviceptr base = 0;
     size_t size = 0;
     const AddrRangeFn range = addr_range_fn();
     if (range == nullptr ||
-        range(&base, &size, reinterpret_cast<CUdeviceptr>(ptrs[key])) != CUDA_SUCCESS)
+        range(&base, &size, reinterpret_cast<CUdeviceptr>(r->local[key])) != CUDA_SUCCESS)
       return set_error(DA_ERR_CUDA, "da_rank: cuMemGetAddressRange failed");
     DA_TRY(ck(cudaIpcGetMemHandle(&rec.handle, reinterpret_cast<void*>(base)),
               "cudaIpcGetMemHandle"));
-    rec.offset = reinterpret_cast<uint64_t>(ptrs[key]) - base;
+    rec.offset = reinterpret_cast<uint64_t>(r->local[key]) - base;
     rec.base = base;
     rec.valid = 1;
   }
@@ -186,40 +384,70 @@ da_status publish(da_rank* r, const std::array<const void*, kNumKeys>& ptrs) {
   return DA_OK;
 }
 
-da_status signal_ready(da_rank* r, int dst, cudaStream_t st) {
-  ++r->sent[dst];
-  return da_stream_write_u32(st, r->flags + dst, r->sent[dst]);
+// Begins a pass: records this pass's buffers, publishes them (IPC).
+da_status begin_pass(da_rank* r) {
+  if (r->world > 1 && r->opts.transport == DA_TRANSPORT_IPC) return publish(r);
+  return DA_OK;
 }
 
-struct Recv {
-  void* slot;
-  size_t bytes;
-  int src;
-  Key key;
-};
+// Receive-slot address of an XRecv (the executor's buffers).
+using SlotFn = void* (*)(da_rank*, const XRecv&);
 
-// Sends (dst per tensor, data produced in stream order on `cur`) and pulls.
-da_status exchange(da_rank* r, const std::vector<int>& sends, const std::vector<Recv>& recvs,
+// Runs one phase: sends + receives of data produced (in stream order) on `cur`.
+da_status exchange(da_rank* r, const Phase& ph, void* (*slot)(da_rank*, const XRecv&),
                    cudaStream_t cur, Work* w) {
   w->expect.clear();
   w->done = nullptr;
-  for (int dst : sends) {
-    DA_TRY(signal_ready(r, dst, cur));
-    w->expect.emplace_back(dst, r->sent[dst]);
+  if (ph.empty()) return DA_OK;
+  const int tr = r->opts.transport;
+  if (tr == DA_TRANSPORT_NONE) {  // fill each slot once from the local buffer of that kind
+    for (const XRecv& x : ph.recvs) {
+      void* dst = slot(r, x);
+      if (r->filled.count(dst)) continue;
+      if (r->local[x.key] == nullptr)
+        return set_error(DA_ERR_STATE, "da_rank: no local buffer for a no-comm slot");
+      DA_TRY(ck(cudaMemcpyAsync(dst, r->local[x.key], r->key_bytes[x.key],
+                                cudaMemcpyDeviceToDevice, cur),
+                "no-comm fill"));
+      r->filled.insert(dst);
+    }
+    return DA_OK;
   }
-  if (recvs.empty()) return DA_OK;
+  if (tr == DA_TRANSPORT_IPC) {
+    for (const XSend& s : ph.sends) {
+      ++r->sent[s.dst];
+      DA_TRY(da_stream_write_u32(cur, r->flags + s.dst, r->sent[s.dst]));
+      w->expect.emplace_back(s.dst, r->sent[s.dst]);
+    }
+    if (ph.recvs.empty()) return DA_OK;
+  }
   cudaEvent_t ready;
   DA_TRY(ck(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event"));
   DA_TRY(ck(cudaEventRecord(ready, cur), "event record"));
   DA_TRY(ck(cudaStreamWaitEvent(r->side, ready, 0), "side wait"));
   cudaEventDestroy(ready);
-  for (const Recv& x : recvs) {
-    const char* src = r->remote[x.src][x.key];
-    if (src == nullptr) return set_error(DA_ERR_STATE, "da_rank: pulled buffer was not published");
-    ++r->pulled[x.src];
-    DA_TRY(da_stream_wait_u32_geq(r->side, r->rflags[x.src] + r->rank, r->pulled[x.src]));
-    DA_TRY(ck(cudaMemcpyAsync(x.slot, src, x.bytes, cudaMemcpyDeviceToDevice, r->side), "pull"));
-    DA_TRY(da_stream_write_u32(r->side, r->flags + r->world + x.src, r->pulled[x.src]));
+  if (tr == DA_TRANSPORT_IPC) {
+    for (const XRecv& x : ph.recvs) {
+      const char* src = r->remote[x.src][x.key];
+      if (src == nullptr)
+        return set_error(DA_ERR_STATE, "da_rank: pulled buffer was not published");
+      ++r->pulled[x.src];
+      DA_TRY(da_stream_wait_u32_geq(r->side, r->rflags[x.src] + r->rank, r->pulled[x.src]));
+      DA_TRY(ck(cudaMemcpyAsync(slot(r, x), src, r->key_bytes[x.key], cudaMemcpyDeviceToDevice,
+                                r->side),
+                "pull"));
+      DA_TRY(da_stream_write_u32(r->side, r->flags + r->world + x.src, r->pulled[x.src]));
+    }
+  } else {  // NCCL: one group per phase, identical phase order on every rank
+    const Nccl& n = nccl();
+    DA_TRY(nk(n.group_start(), "ncclGroupStart"));
+    for (const XSend& s : ph.sends)
+      DA_TRY(nk(n.send(r->local[s.key], r->key_bytes[s.key], ncclUint8, s.dst, r->comm, r->side),
+                "ncclSend"));
+    for (const XRecv& x : ph.recvs)
+      DA_TRY(nk(n.recv(slot(r, x), r->key_bytes[x.key], ncclUint8, x.src, r->comm, r->side),
+                "ncclRecv"));
+    DA_TRY(nk(n.group_end(), "ncclGroupEnd"));
   }
   DA_TRY(ck(cudaEventCreateWithFlags(&w->done, cudaEventDisableTiming), "event"));
   return ck(cudaEventRecord(w->done, r->side), "event record");
@@ -227,7 +455,7 @@ da_status exchange(da_rank* r, const std::vector<int>& sends, const std::vector<
 
 da_status wait_work(da_rank* r, Work* w, cudaStream_t cur) {
   if (w->done) {
-    DA_TRY(ck(cudaStreamWaitEvent(cur, w->done, 0), "wait pulls"));
+    DA_TRY(ck(cudaStreamWaitEvent(cur, w->done, 0), "wait transfers"));
     cudaEventDestroy(w->done);
     w->done = nullptr;
   }
@@ -235,38 +463,6 @@ da_status wait_work(da_rank* r, Work* w, cudaStream_t cur) {
     DA_TRY(da_stream_wait_u32_geq(cur, r->rflags[e.first] + r->world + r->rank, e.second));
   w->expect.clear();
   return DA_OK;
-}
-
-struct Plan {
-  int action = 0;  // 0 idle, 1 local, 2 direct, 3 help
-  int peer = 0;    // 1-based
-  int part = kPartWhole;
-  std::vector<int> kv_sends, kvh_sends, q_sends, merges, gradkv_from;
-};
-
-std::vector<Plan> plans_for(const FlatSchedule& s, int worker) {
-  std::vector<Plan> plans(s.steps);
-  for (const Task& k : s.tasks) {
-    if (k.worker != worker) continue;
-    Plan& p = plans[k.step];
-    if (k.kind == kLocal) {
-      p.action = 1;
-    } else if (k.kind == kRemote) {
-      p.action = k.query_owner == worker ? 2 : 3;
-      p.peer = k.query_owner == worker ? k.kv_owner : k.query_owner;
-      p.part = k.helper;
-    } else if (k.kind == kMerge) {
-      p.merges.push_back(k.helper);
-    }
-  }
-  for (const Message& m : s.messages) {
-    Plan& p = plans[m.step];
-    if (m.from == worker && m.kind == kMsgKV) p.kv_sends.push_back(m.to);
-    if (m.from == worker && m.kind == kMsgKVHalf) p.kvh_sends.push_back(m.to);
-    if (m.from == worker && m.kind == kMsgQ) p.q_sends.push_back(m.to);
-    if (m.to == worker && m.kind == kMsgGradKV) p.gradkv_from.push_back(m.from);
-  }
-  return plans;
 }
 
 da_status fwd_chunk(const void* q, const void* k, const void* v, int64_t h_q, int64_t h_kv,
@@ -297,7 +493,7 @@ da_status fwd_chunk(const void* q, const void* k, const void* v, int64_t h_q, in
 da_status bwd_chunk(const void* q, const void* k, const void* v, const void* d_out,
                     const float* lse, const float* d_vec, int64_t h_q, int64_t h_kv, int64_t rows,
                     float* dq, float* dk, float* dv, bool accumulate_kv, int mask,
-                    cudaStream_t st) {
+                    bool deterministic, cudaStream_t st) {
   da_bwd_args a{};
   a.q = q;
   a.k = k;
@@ -315,6 +511,7 @@ da_status bwd_chunk(const void* q, const void* k, const void* v, const void* d_o
   a.dv_acc = dv;
   a.accumulate_kv = accumulate_kv ? 1 : 0;
   a.mask = mask;
+  a.deterministic = deterministic ? 1 : 0;
   return da_attn_bwd_chunk(&a, st);
 }
 
@@ -334,6 +531,51 @@ void count(da_counters& c, int kind, int64_t scalars) {
   }
 }
 
+FlatSchedule forward_table(int kind, int P, bool* ok) {
+  *ok = true;
+  if (kind == DA_SCHEDULE_RING) return make_ring(P);
+  if (kind == DA_SCHEDULE_BALANCED) return make_balanced(P);
+  if (kind == DA_SCHEDULE_BALANCED_SPLIT) return make_balanced_split(P);
+  *ok = false;
+  return FlatSchedule{};
+}
+
+FlatSchedule backward_table(int kind, int P, bool* ok) {
+  *ok = true;
+  if (kind == DA_SCHEDULE_RING_BWD || kind == DA_SCHEDULE_RING) return make_ring_backward(P);
+  if (kind == DA_SCHEDULE_BALANCED_BWD || kind == DA_SCHEDULE_BALANCED)
+    return make_balanced_backward(P);
+  *ok = false;
+  return FlatSchedule{};
+}
+
+// receive-slot resolution of the two passes
+void* fwd_slot(da_rank* r, const XRecv& x) {
+  const size_t kv_b = static_cast<size_t>(r->h_kv) * r->rows * 256;
+  const size_t half_b = r->key_bytes[kKHi];
+  switch (x.slot) {
+    case kSlotKV: return r->kv_slot[x.index].as<char>() + x.part * kv_b;
+    case kSlotKVH: return r->kvh.as<char>() + x.part * half_b;
+    case kSlotQ: return r->q_slot[x.index].p;
+    case kSlotPart: return r->part_recv[x.index].p;
+    default: return nullptr;
+  }
+}
+
+void* bwd_slot(da_rank* r, const XRecv& x) {
+  const int64_t nq = r->h_q * r->rows, nkv = r->h_kv * r->rows;
+  const size_t kv_b = static_cast<size_t>(nkv) * 256, q_b = static_cast<size_t>(nq) * 256;
+  const size_t g_kv = static_cast<size_t>(nkv) * 128 * 4;
+  const size_t bundle_off[4] = {0, q_b, 2 * q_b, 2 * q_b + static_cast<size_t>(nq) * 4};
+  switch (x.slot) {
+    case kSlotKV: return r->kv_slot[x.index].as<char>() + x.part * kv_b;
+    case kSlotBundle: return r->bundle[x.index].as<char>() + bundle_off[x.part];
+    case kSlotGrad: return r->g_recv.as<char>() + x.part * g_kv;
+    case kSlotGQ: return r->gq_recv[x.index].p;
+    default: return nullptr;
+  }
+}
+
 }  // namespace
 }  // namespace da
 
@@ -341,48 +583,78 @@ using namespace da;
 
 extern "C" {
 
-da_status da_rank_create(int rank, int world, da_allgather_fn fn, void* ctx, da_rank** out) {
+da_status da_rank_create_ex(int rank, int world, da_allgather_fn fn, void* ctx,
+                            const da_rank_options* opts, da_rank** out) {
   if (out == nullptr || fn == nullptr) return set_error(DA_ERR_CONFIG, "da_rank_create: null");
   if (world < 1 || rank < 0 || rank >= world)
     return set_error(DA_ERR_CONFIG, "da_rank_create: bad rank / world");
   std::unique_ptr<da_rank> r(new da_rank());
   r->rank = rank;
   r->world = world;
+  if (opts) r->opts = *opts;
+  const int tr = r->opts.transport;
+  if (tr != DA_TRANSPORT_IPC && tr != DA_TRANSPORT_NCCL && tr != DA_TRANSPORT_NONE)
+    return set_error(DA_ERR_CONFIG, "da_rank_create: unknown transport");
   r->ag = fn;
   r->ctx = ctx;
   r->sent.assign(world, 0);
   r->pulled.assign(world, 0);
   r->remote.assign(world, {});
   for (auto& a : r->remote) a.fill(nullptr);
-  DA_TRY(ck(cudaStreamCreateWithFlags(&r->side, cudaStreamNonBlocking), "side stream"));
-  DA_TRY(ck(cudaMalloc(&r->flags, sizeof(int) * 2 * world), "flags"));
-  DA_TRY(ck(cudaMemset(r->flags, 0, sizeof(int) * 2 * world), "flags"));
-  r->rflags.assign(world, r->flags);
-  // exchange the flag pages once
-  std::vector<PubRecord> mine(1), all(world);
-  std::memset(mine.data(), 0, sizeof(PubRecord));
-  DA_TRY(ck(cudaIpcGetMemHandle(&mine[0].handle, r->flags), "cudaIpcGetMemHandle(flags)"));
-  mine[0].valid = 1;
-  if (world > 1) {
-    if (fn(ctx, mine.data(), sizeof(PubRecord), all.data()) != 0)
-      return set_error(DA_ERR_CONFIG, "da_rank_create: allgather callback failed");
-    for (int s = 0; s < world; ++s) {
-      if (s == rank) continue;
-      void* p = nullptr;
-      DA_TRY(ck(cudaIpcOpenMemHandle(&p, all[s].handle, cudaIpcMemLazyEnablePeerAccess),
-                "cudaIpcOpenMemHandle(flags)"));
-      r->rflags[s] = static_cast<int*>(p);
+  int lo = 0, hi = 0;  // transfers overtake kernels on the side stream
+  DA_TRY(ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priorities"));
+  DA_TRY(ck(cudaStreamCreateWithPriority(&r->side, cudaStreamNonBlocking, hi), "side stream"));
+  if (tr == DA_TRANSPORT_IPC) {
+    DA_TRY(ck(cudaMalloc(&r->flags, sizeof(int) * 2 * world), "flags"));
+    DA_TRY(ck(cudaMemset(r->flags, 0, sizeof(int) * 2 * world), "flags"));
+    r->rflags.assign(world, r->flags);
+    std::vector<PubRecord> mine(1), all(world);
+    std::memset(mine.data(), 0, sizeof(PubRecord));
+    DA_TRY(ck(cudaIpcGetMemHandle(&mine[0].handle, r->flags), "cudaIpcGetMemHandle(flags)"));
+    mine[0].valid = 1;
+    if (world > 1) {
+      if (fn(ctx, mine.data(), sizeof(PubRecord), all.data()) != 0)
+        return set_error(DA_ERR_CONFIG, "da_rank_create: allgather callback failed");
+      for (int s = 0; s < world; ++s) {
+        if (s == rank) continue;
+        void* p = nullptr;
+        DA_TRY(ck(cudaIpcOpenMemHandle(&p, all[s].handle, cudaIpcMemLazyEnablePeerAccess),
+                  "cudaIpcOpenMemHandle(flags)"));
+        r->rflags[s] = static_cast<int*>(p);
+      }
     }
+  } else if (tr == DA_TRANSPORT_NCCL) {
+    const Nccl& n = nccl();
+    if (!n.ok) return set_error(DA_ERR_NCCL, "da_rank_create: libnccl.so.2 not loadable");
+    ncclUniqueId id;
+    std::memset(&id, 0, sizeof(id));
+    if (rank == 0) DA_TRY(nk(n.get_unique_id(&id), "ncclGetUniqueId"));
+    std::vector<ncclUniqueId> ids(world);
+    if (fn(ctx, &id, sizeof(id), ids.data()) != 0)
+      return set_error(DA_ERR_CONFIG, "da_rank_create: allgather callback failed");
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    if (r->opts.nccl_max_ctas > 0) {
+      cfg.minCTAs = 1;
+      cfg.maxCTAs = r->opts.nccl_max_ctas;
+    }
+    DA_TRY(nk(n.init_rank_config(&r->comm, world, ids[0], rank, &cfg), "ncclCommInitRankConfig"));
   }
   *out = r.release();
   return DA_OK;
 }
 
+da_status da_rank_create(int rank, int world, da_allgather_fn fn, void* ctx, da_rank** out) {
+  da_rank_options o{};
+  o.transport = DA_TRANSPORT_IPC;
+  return da_rank_create_ex(rank, world, fn, ctx, &o, out);
+}
+
 void da_rank_destroy(da_rank* r) {
   if (r == nullptr) return;
   cudaDeviceSynchronize();
+  if (r->comm) nccl().destroy(r->comm);
   for (auto& kv : r->opened) cudaIpcCloseMemHandle(kv.second);
-  for (int s = 0; s < r->world; ++s)
+  for (int s = 0; s < static_cast<int>(r->rflags.size()); ++s)
     if (r->rflags[s] != r->flags) cudaIpcCloseMemHandle(r->rflags[s]);
   if (r->flags) cudaFree(r->flags);
   if (r->side) cudaStreamDestroy(r->side);
@@ -396,15 +668,19 @@ da_status da_rank_forward(da_rank* r, int schedule_kind, const void* q, const vo
   if (h_q < 1 || h_kv < 1 || h_q % h_kv != 0 || rows < 1)
     return set_error(DA_ERR_SHAPE, "da_rank_forward: bad shape");
   const int P = r->world, w = r->rank + 1;
-  FlatSchedule sch;
-  if (schedule_kind == DA_SCHEDULE_RING) sch = make_ring(P);
-  else if (schedule_kind == DA_SCHEDULE_BALANCED) sch = make_balanced(P);
-  else if (schedule_kind == DA_SCHEDULE_BALANCED_SPLIT) sch = make_balanced_split(P);
-  else return set_error(DA_ERR_CONFIG, "da_rank_forward: unknown schedule kind");
+  bool ok = false;
+  const FlatSchedule sch = forward_table(schedule_kind, P, &ok);
+  if (!ok) return set_error(DA_ERR_CONFIG, "da_rank_forward: unknown schedule kind");
   const auto errs = validate_flat(sch);
   if (!errs.empty()) return set_error(DA_ERR_SCHEDULE, "invalid schedule: " + errs.front());
-  const auto plans = plans_for(sch, w);
+  Program pg;
+  DA_TRY(forward_program(sch, w, &pg));
+  const auto& plans = pg.plans;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  r->h_q = h_q;
+  r->h_kv = h_kv;
+  r->rows = rows;
+  r->have_forward = false;
   const int64_t nq = h_q * rows, nkv = h_kv * rows;
   const size_t acc_f = static_cast<size_t>(nq) * 130;  // o | m | l
   const size_t kv_b = static_cast<size_t>(nkv) * 256, q_b = static_cast<size_t>(nq) * 256;
@@ -420,9 +696,9 @@ da_status da_rank_forward(da_rank* r, int schedule_kind, const void* q, const vo
   for (const Plan& p : plans) split = split || p.part != kPartWhole || !p.kvh_sends.empty();
   if (split) {
     DA_TRY(ck(r->k_lo.ensure(static_cast<size_t>(h_kv) * (lo > 0 ? lo : 1) * 256),
-       "da_rank workspace"));
+              "da_rank workspace"));
     DA_TRY(ck(r->v_lo.ensure(static_cast<size_t>(h_kv) * (lo > 0 ? lo : 1) * 256),
-       "da_rank workspace"));
+              "da_rank workspace"));
     DA_TRY(ck(r->k_hi.ensure(static_cast<size_t>(h_kv) * hi * 256), "da_rank workspace"));
     DA_TRY(ck(r->v_hi.ensure(static_cast<size_t>(h_kv) * hi * 256), "da_rank workspace"));
     DA_TRY(ck(r->kvh.ensure(2 * static_cast<size_t>(h_kv) * hi * 256), "da_rank workspace"));
@@ -433,50 +709,38 @@ da_status da_rank_forward(da_rank* r, int schedule_kind, const void* q, const vo
     if (e == cudaSuccess) e = pack_rows(v, r->v_hi.p, h_kv, rows, lo, hi, st);
     DA_TRY(ck(e, "da_rank_forward split pack"));
   }
-  std::array<const void*, kNumKeys> pub{};
-  pub.fill(nullptr);
-  pub[kK] = k;
-  pub[kV] = v;
-  pub[kQ] = q;
-  pub[kPart] = r->part.p;
+  for (const Plan& p : plans)
+    for (int hw : p.merges) DA_TRY(ck(r->part_recv[hw].ensure(acc_f * 4), "da_rank workspace"));
+  r->local.fill(nullptr);
+  r->key_bytes.fill(0);
+  r->local[kK] = k;
+  r->local[kV] = v;
+  r->local[kQ] = q;
+  r->local[kPart] = r->part.p;
+  r->key_bytes[kK] = r->key_bytes[kV] = kv_b;
+  r->key_bytes[kQ] = q_b;
+  r->key_bytes[kPart] = acc_f * 4;
   if (split) {
-    pub[kKHi] = r->k_hi.p;
-    pub[kVHi] = r->v_hi.p;
+    r->local[kKHi] = r->k_hi.p;
+    r->local[kVHi] = r->v_hi.p;
+    r->key_bytes[kKHi] = r->key_bytes[kVHi] = static_cast<size_t>(h_kv) * hi * 256;
   }
-  if (P > 1) DA_TRY(publish(r, pub));
+  if (P > 1) DA_TRY(begin_pass(r));
 
   da_counters c{};
   float* acc = r->acc.as<float>();
   bool have_acc = false;
-  auto post = [&](int t, Work* work) -> da_status {
-    const Plan& p = plans[t];
-    std::vector<int> sends;
-    std::vector<Recv> recvs;
-    for (int dst : p.kv_sends) sends.insert(sends.end(), {dst - 1, dst - 1});
-    for (int dst : p.kvh_sends) sends.insert(sends.end(), {dst - 1, dst - 1});
-    for (int dst : p.q_sends) sends.push_back(dst - 1);
-    if (p.action == 2 && p.part == kPartHigh) {
-      recvs.push_back({r->kvh.p, static_cast<size_t>(h_kv) * hi * 256, p.peer - 1, kKHi});
-      recvs.push_back({r->kvh.as<char>() + static_cast<size_t>(h_kv) * hi * 256,
-                       static_cast<size_t>(h_kv) * hi * 256, p.peer - 1, kVHi});
-    } else if (p.action == 2) {
-      recvs.push_back({r->kv_slot[t % 2].p, kv_b, p.peer - 1, kK});
-      recvs.push_back({r->kv_slot[t % 2].as<char>() + kv_b, kv_b, p.peer - 1, kV});
-    } else if (p.action == 3) {
-      recvs.push_back({r->q_slot[t % 2].p, q_b, p.peer - 1, kQ});
-    }
-    return exchange(r, sends, recvs, st, work);
-  };
-
   Work pending, part_work;
   bool part_pending = false;
   int held = 0;
-  if (P > 1) DA_TRY(post(0, &pending));
-  for (int t = 0; t < static_cast<int>(plans.size()); ++t) {
+  const int T = static_cast<int>(plans.size());
+  if (P > 1) DA_TRY(exchange(r, pg.operands[0], fwd_slot, st, &pending));
+  for (int t = 0; t < T; ++t) {
     const Plan& p = plans[t];
     Work next;
-    const bool has_next = t + 1 < static_cast<int>(plans.size());
-    if (has_next) DA_TRY(post(t + 1, &next));  // prefetch: overlaps this step's compute
+    const bool has_next = t + 1 < T;
+    if (has_next && P > 1)  // prefetch: overlaps this step's compute
+      DA_TRY(exchange(r, pg.operands[t + 1], fwd_slot, st, &next));
     DA_TRY(wait_work(r, &pending, st));
     const int cur_held = (p.action >= 2 ? 1 : 0) + (has_next && plans[t + 1].action >= 2 ? 1 : 0);
     held = cur_held > held ? cur_held : held;
@@ -497,21 +761,24 @@ da_status da_rank_forward(da_rank* r, int schedule_kind, const void* q, const vo
     } else if (p.action == 3) {
       ++c.attention_kernel_calls;
       count(c, kMsgQ, nq * 128);
-      if (part_pending) DA_TRY(wait_work(r, &part_work, st));  // previous partial pulled
+      if (part_pending) DA_TRY(wait_work(r, &part_work, st));  // previous partial has left
+      part_pending = false;
       const bool low = p.part == kPartLow;
       DA_TRY(fwd_chunk(r->q_slot[t % 2].p, low ? r->k_lo.p : k, low ? r->v_lo.p : v, h_q, h_kv,
                        rows, low ? lo : rows, nullptr, r->part.as<float>(), DA_MASK_FULL, st));
-      DA_TRY(exchange(r, {p.peer - 1}, {}, st, &part_work));
-      part_pending = true;
     }
-    for (int hw : p.merges) {
-      da::Buf& buf = r->part_recv[hw];
-      DA_TRY(ck(buf.ensure(acc_f * 4), "da_rank workspace"));
-      Work mw;
-      DA_TRY(exchange(r, {}, {{buf.p, acc_f * 4, hw - 1, kPart}}, st, &mw));
-      DA_TRY(wait_work(r, &mw, st));
+    Work res;
+    if (P > 1) DA_TRY(exchange(r, pg.results[t], fwd_slot, st, &res));
+    if (p.action == 3 && p.merges.empty()) {
+      part_work = res;  // the partial's send completes before r->part is rewritten
+      part_pending = true;
+    } else {
+      DA_TRY(wait_work(r, &res, st));  // partials from this step's helpers have landed
+      part_pending = false;
+    }
+    for (int hw : p.merges) {  // in helper order (runtime.cpp:322-328, 468-474)
       count(c, kMsgPartial, nq * 130);
-      const float* b = buf.as<float>();
+      const float* b = r->part_recv[hw].as<float>();
       DA_TRY(ck(launch_merge(acc, acc + nq * 128, acc + nq * 129, b, b + nq * 128, b + nq * 129,
                              acc, acc + nq * 128, acc + nq * 129, nq, st),
                 "da_rank_forward merge"));
@@ -528,12 +795,10 @@ da_status da_rank_forward(da_rank* r, int schedule_kind, const void* q, const vo
   r->v = v;
   r->out = out;
   r->lse = lse;
-  r->h_q = h_q;
-  r->h_kv = h_kv;
-  r->rows = rows;
   r->have_forward = true;
   c.max_remote_chunks_held = held;
   if (counters) *counters = c;
+  if (r->opts.transport == DA_TRANSPORT_NONE) return DA_OK;  // garbage-in by design
   return da_check_degenerate(r->flag.as<int>(), stream);
 }
 
@@ -544,17 +809,16 @@ da_status da_rank_backward(da_rank* r, int schedule_kind, const void* d_out, flo
     return set_error(DA_ERR_STATE, "run_backward requires forward output and logsumexp");
   if (d_out == nullptr) return set_error(DA_ERR_STATE, "run_backward requires d_out");
   const int P = r->world, w = r->rank + 1;
-  FlatSchedule sch;
-  if (schedule_kind == DA_SCHEDULE_RING_BWD || schedule_kind == DA_SCHEDULE_RING)
-    sch = make_ring_backward(P);
-  else if (schedule_kind == DA_SCHEDULE_BALANCED_BWD || schedule_kind == DA_SCHEDULE_BALANCED)
-    sch = make_balanced_backward(P);
-  else
-    return set_error(DA_ERR_CONFIG, "da_rank_backward: unknown schedule kind");
+  bool ok = false;
+  const FlatSchedule sch = backward_table(schedule_kind, P, &ok);
+  if (!ok) return set_error(DA_ERR_CONFIG, "da_rank_backward: unknown schedule kind");
   const auto errs = validate_backward_flat(sch);
   if (!errs.empty()) return set_error(DA_ERR_SCHEDULE, "invalid schedule: " + errs.front());
-  const auto plans = plans_for(sch, w);
+  Program pg;
+  DA_TRY(backward_program(sch, w, &pg));
+  const auto& plans = pg.plans;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool det = r->opts.deterministic != 0;
   const int64_t h_q = r->h_q, h_kv = r->h_kv, rows = r->rows;
   const int64_t nq = h_q * rows, nkv = h_kv * rows;
   const size_t kv_b = static_cast<size_t>(nkv) * 256, q_b = static_cast<size_t>(nq) * 256;
@@ -568,65 +832,53 @@ da_status da_rank_backward(da_rank* r, int schedule_kind, const void* d_out, flo
     DA_TRY(ck(r->q_send[i].ensure(g_q), "da_rank workspace"));
   }
   DA_TRY(ck(r->g_recv.ensure(2 * g_kv), "da_rank workspace"));
+  for (const Plan& p : plans)
+    for (int hw : p.merges) DA_TRY(ck(r->gq_recv[hw].ensure(g_q), "da_rank workspace"));
   DA_TRY(ck(cudaMemsetAsync(dq, 0, g_q, st), "dq zero"));
   DA_TRY(ck(cudaMemsetAsync(dk, 0, g_kv, st), "dk zero"));
   DA_TRY(ck(cudaMemsetAsync(dv, 0, g_kv, st), "dv zero"));
   DA_TRY(ck(launch_bwd_preprocess(d_out, r->out, r->d_vec.as<float>(), nq, st), "preprocess"));
-  std::array<const void*, kNumKeys> pub{};
-  pub.fill(nullptr);
-  pub[kK] = r->k;
-  pub[kV] = r->v;
-  pub[kQ] = r->q;
-  pub[kDOut] = d_out;
-  pub[kLse] = r->lse;
-  pub[kDVec] = r->d_vec.p;
-  pub[kGK0] = r->g_send[0].p;
-  pub[kGV0] = r->g_send[0].as<char>() + g_kv;
-  pub[kGK1] = r->g_send[1].p;
-  pub[kGV1] = r->g_send[1].as<char>() + g_kv;
-  pub[kGQ0] = r->q_send[0].p;
-  pub[kGQ1] = r->q_send[1].p;
-  if (P > 1) DA_TRY(publish(r, pub));
+  r->local.fill(nullptr);
+  r->key_bytes.fill(0);
+  r->local[kK] = r->k;
+  r->local[kV] = r->v;
+  r->local[kQ] = r->q;
+  r->local[kDOut] = d_out;
+  r->local[kLse] = r->lse;
+  r->local[kDVec] = r->d_vec.p;
+  r->local[kGK0] = r->g_send[0].p;
+  r->local[kGV0] = r->g_send[0].as<char>() + g_kv;
+  r->local[kGK1] = r->g_send[1].p;
+  r->local[kGV1] = r->g_send[1].as<char>() + g_kv;
+  r->local[kGQ0] = r->q_send[0].p;
+  r->local[kGQ1] = r->q_send[1].p;
+  r->key_bytes[kK] = r->key_bytes[kV] = kv_b;
+  r->key_bytes[kQ] = r->key_bytes[kDOut] = q_b;
+  r->key_bytes[kLse] = r->key_bytes[kDVec] = static_cast<size_t>(nq) * 4;
+  for (Key key : {kGK0, kGV0, kGK1, kGV1}) r->key_bytes[key] = g_kv;
+  r->key_bytes[kGQ0] = r->key_bytes[kGQ1] = g_q;
+  if (P > 1) DA_TRY(begin_pass(r));
 
   da_counters c{};
-  auto post = [&](int t, Work* work) -> da_status {
-    const Plan& p = plans[t];
-    std::vector<int> sends;
-    std::vector<Recv> recvs;
-    for (int dst : p.kv_sends) sends.insert(sends.end(), {dst - 1, dst - 1});
-    for (int dst : p.q_sends) sends.insert(sends.end(), {dst - 1, dst - 1, dst - 1, dst - 1});
-    if (p.action == 2) {
-      recvs.push_back({r->kv_slot[t % 2].p, kv_b, p.peer - 1, kK});
-      recvs.push_back({r->kv_slot[t % 2].as<char>() + kv_b, kv_b, p.peer - 1, kV});
-    } else if (p.action == 3) {
-      char* b = r->bundle[t % 2].as<char>();
-      recvs.push_back({b, q_b, p.peer - 1, kQ});
-      recvs.push_back({b + q_b, q_b, p.peer - 1, kDOut});
-      recvs.push_back({b + 2 * q_b, static_cast<size_t>(nq) * 4, p.peer - 1, kLse});
-      recvs.push_back({b + 2 * q_b + nq * 4, static_cast<size_t>(nq) * 4, p.peer - 1, kDVec});
-    }
-    return exchange(r, sends, recvs, st, work);
-  };
   Work pending;
-  if (P > 1) DA_TRY(post(0, &pending));
-  for (int t = 0; t < static_cast<int>(plans.size()); ++t) {
+  const int T = static_cast<int>(plans.size());
+  if (P > 1) DA_TRY(exchange(r, pg.operands[0], bwd_slot, st, &pending));
+  for (int t = 0; t < T; ++t) {
     const Plan& p = plans[t];
     Work next;
-    if (t + 1 < static_cast<int>(plans.size())) DA_TRY(post(t + 1, &next));
+    if (t + 1 < T && P > 1) DA_TRY(exchange(r, pg.operands[t + 1], bwd_slot, st, &next));
     DA_TRY(wait_work(r, &pending, st));
-    std::vector<int> sends;
     if (p.action == 1) {
       ++c.attention_kernel_calls;
       DA_TRY(bwd_chunk(r->q, r->k, r->v, d_out, r->lse, r->d_vec.as<float>(), h_q, h_kv, rows, dq,
-                       dk, dv, true, DA_MASK_DIAGONAL, st));
+                       dk, dv, true, DA_MASK_DIAGONAL, det, st));
     } else if (p.action == 2) {
       ++c.attention_kernel_calls;
       count(c, kMsgKV, 2 * nkv * 128);
       const char* ks = r->kv_slot[t % 2].as<char>();
       float* gk = r->g_send[t % 2].as<float>();
       DA_TRY(bwd_chunk(r->q, ks, ks + kv_b, d_out, r->lse, r->d_vec.as<float>(), h_q, h_kv, rows,
-                       dq, gk, gk + nkv * 128, false, DA_MASK_FULL, st));
-      sends.insert(sends.end(), {p.peer - 1, p.peer - 1});
+                       dq, gk, gk + nkv * 128, false, DA_MASK_FULL, det, st));
     } else if (p.action == 3) {
       ++c.attention_kernel_calls;
       c.q_scalars += rows * (2 * 128 + 2) * h_q;
@@ -636,27 +888,12 @@ da_status da_rank_backward(da_rank* r, int schedule_kind, const void* d_out, flo
       DA_TRY(ck(cudaMemsetAsync(gq, 0, g_q, st), "gq zero"));
       DA_TRY(bwd_chunk(b, r->k, r->v, b + q_b, reinterpret_cast<const float*>(b + 2 * q_b),
                        reinterpret_cast<const float*>(b + 2 * q_b + nq * 4), h_q, h_kv, rows, gq,
-                       dk, dv, true, DA_MASK_FULL, st));
-      sends.push_back(p.peer - 1);
-    }
-    if (p.gradkv_from.size() > 1)
-      return set_error(DA_ERR_SCHEDULE, "at most one GradKV per worker and step is supported");
-    std::vector<Recv> recvs;
-    const Key gk_key = (t % 2) ? kGK1 : kGK0, gv_key = (t % 2) ? kGV1 : kGV0;
-    const Key gq_key = (t % 2) ? kGQ1 : kGQ0;
-    for (int s : p.gradkv_from) {
-      recvs.push_back({r->g_recv.p, g_kv, s - 1, gk_key});
-      recvs.push_back({r->g_recv.as<char>() + g_kv, g_kv, s - 1, gv_key});
-    }
-    for (int hw : p.merges) {
-      da::Buf& buf = r->gq_recv[hw];
-      DA_TRY(ck(buf.ensure(g_q), "da_rank workspace"));
-      recvs.push_back({buf.p, g_q, hw - 1, gq_key});
+                       dk, dv, true, DA_MASK_FULL, det, st));
     }
     // results leave right after their kernels; waiting also retires the send
     // buffers before they are rewritten two steps later
     Work sw;
-    DA_TRY(exchange(r, sends, recvs, st, &sw));
+    if (P > 1) DA_TRY(exchange(r, pg.results[t], bwd_slot, st, &sw));
     DA_TRY(wait_work(r, &sw, st));
     if (!p.gradkv_from.empty()) {
       count(c, kMsgGradKV, 2 * nkv * 128);
@@ -671,6 +908,42 @@ da_status da_rank_backward(da_rank* r, int schedule_kind, const void* d_out, flo
     pending = next;
   }
   if (counters) *counters = c;
+  return DA_OK;
+}
+
+// The pass's phase lists of one rank, without a device (protocol tests):
+// per entry {pass (0 fwd, 1 bwd), phase (2t + 0 operands(t), 2t + 1
+// results(t)), dir (0 send, 1 recv), peer (0-based), key}.
+da_status da_rank_protocol(int world, int rank, int fwd_kind, int bwd_kind, int32_t* out,
+                           int64_t cap, int64_t* n) {
+  if (n == nullptr || world < 1 || rank < 0 || rank >= world)
+    return set_error(DA_ERR_CONFIG, "da_rank_protocol: bad arguments");
+  *n = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    bool ok = false;
+    const FlatSchedule sch = pass == 0 ? forward_table(fwd_kind, world, &ok)
+                                       : backward_table(bwd_kind, world, &ok);
+    if (!ok) return set_error(DA_ERR_CONFIG, "da_rank_protocol: unknown schedule kind");
+    Program pg;
+    DA_TRY(pass == 0 ? forward_program(sch, rank + 1, &pg) : backward_program(sch, rank + 1, &pg));
+    for (size_t t = 0; t < pg.plans.size(); ++t)
+      for (int kind = 0; kind < 2; ++kind) {
+        const Phase& ph = kind == 0 ? pg.operands[t] : pg.results[t];
+        auto emit = [&](int dir, int peer, int key) {
+          if (out != nullptr && *n < cap) {
+            int32_t* e = out + 5 * (*n);
+            e[0] = pass;
+            e[1] = static_cast<int32_t>(2 * t + kind);
+            e[2] = dir;
+            e[3] = peer;
+            e[4] = key;
+          }
+          ++*n;
+        };
+        for (const XSend& s : ph.sends) emit(0, s.dst, s.key);
+        for (const XRecv& x : ph.recvs) emit(1, x.src, x.key);
+      }
+  }
   return DA_OK;
 }
 

@@ -22,14 +22,26 @@ _BWD = {"ring": 2, "balanced": 3}
 
 
 class RankRuntime:
-    """One rank of the sequence-parallel runtime; all calls are collective."""
+    """One rank of the sequence-parallel runtime; all calls are collective.
 
-    def __init__(self, rank: int, world: int, group=None):
+    transport: "nccl" (grouped send/recv per phase on a side stream; ranks on
+    distinct GPUs), "ipc" (copy-engine pulls from peer HBM; ranks may share a
+    GPU) or "none" (no transfer: the no-communication timing arm).
+    deterministic: ordered dq reductions, bitwise-reproducible backward."""
+
+    def __init__(self, rank: int, world: int, group=None, transport: str = "ipc",
+                 deterministic: bool = False, nccl_max_ctas: int = 0):
+        from .errors import ConfigError
+        if transport not in _lib.TRANSPORT:
+            raise ConfigError(f"unknown transport {transport!r}")
         self.rank, self.world, self.group = rank, world, group
+        self.transport, self.deterministic = transport, deterministic
         self._cb = _AG(self._allgather)  # keep the trampoline alive
+        opts = _lib.RankOptions(_lib.TRANSPORT[transport], 1 if deterministic else 0,
+                                int(nccl_max_ctas))
         h = C.c_void_p()
-        check(_lib.lib().da_rank_create(rank, world, C.cast(self._cb, C.c_void_p), None,
-                                        C.byref(h)))
+        check(_lib.lib().da_rank_create_ex(rank, world, C.cast(self._cb, C.c_void_p), None,
+                                           C.byref(opts), C.byref(h)))
         self._h = h
         self._saved = None
 

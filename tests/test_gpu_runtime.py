@@ -220,8 +220,9 @@ def test_runtime_takes_any_valid_schedule_table(cuda):
     run_backward(same, S.build_ring_backward_schedule(4))
     got = outs(same)
     assert torch.equal(got[0], ref[0]) and torch.equal(got[1], ref[1])
-    for f, r in zip(("dq", "dk", "dv"), ref_g):
-        assert torch.equal(torch.cat([getattr(x, f) for x in same], 1), r), f
+    for f, r in zip(("dq", "dk", "dv"), ref_g):  # dq: unordered fp32 reductions by default
+        g = torch.cat([getattr(x, f) for x in same], 1)
+        assert (torch.equal(g, r) if f != "dq" else rel_err(g, r) < 1e-5), f
 
     custom = S.build_ring_schedule(4)
     custom.steps[1], custom.steps[2] = custom.steps[2], custom.steps[1]
