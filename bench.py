@@ -1,24 +1,33 @@
 """Benchmark: causal attention forward+backward (DistFlashAttn hot path) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg2|cfg2gqa|cfg3|cfg4|cfg5]
 
-N=1 workload = BASELINE.json configs[1]: Llama-7B attention layer (32 heads,
-d=128), causal fwd+bwd at seq 32K on one B200, synthetic U[-1,1) bf16 inputs
-generated on the device. One step = one forward (block_attn_update with the
-fused finalize) + backward_aux + block_attn_backward over the full sequence.
-N>1 runs the sequence-parallel runtime (paper_2310_03294_b200/dist.py): the
-sequence is split into N contiguous chunks, one per rank (32K tokens per GPU),
-balanced forward + balanced backward schedules, messages pulled by the copy
-engines from the peers' HBM (--transport peer, default) or NCCL send/recv.
+N=1 workload = BASELINE.json configs[1] (cfg2): Llama-7B attention layer (32
+heads, d=128), causal fwd+bwd at seq 32K on one B200, synthetic U[-1,1) bf16
+inputs generated on the device. One step = one forward (block_attn_update
+with the fused finalize) + backward_aux + block_attn_backward over the full
+sequence. `--config cfg2gqa` is the same with 8 kv heads (cfg5's ratio).
+
+N>1 (configs[2..4]; default cfg3 = 128K tokens over N GPUs, strong scaling)
+runs the native per-rank runtime (csrc/rank_runtime.cu), one process per GPU:
+plain `python bench.py --gpus N` spawns its N ranks itself (torchrun works
+too). The headline leg is the balanced forward with the even-P split +
+balanced backward; the same line carries the ring/ring and balanced/balanced
+legs (the north_star balanced-vs-ring speed-up) and a no-communication leg
+(same kernels on local buffers) from which exposed communication is
+computed as the reference's comm_overhead_pct (analyzer.cpp:60-64).
+Transport: NCCL send/recv on a side stream when the ranks sit on distinct
+GPUs, CUDA-IPC copy-engine pulls when they share one (--share-gpu, tests).
 
 Metric: whole-job attention fwd+bwd TFLOP/s (algorithmic causal FLOPs
 7·N²·d·H per step, no recompute counted), with tokens/s and per-GPU TFLOP/s
-beside it. Inputs (4 × 268 MB at 32K) exceed the 126 MB L2, so no flush is
-needed between steps.
+beside it. Inputs exceed the 126 MB L2 at every config, so no flush is needed
+between steps.
 
 --impl reference times the reference's own CPU implementation (the
 unmodified sources compiled into oracle/_ref/ref_driver) on a bounded sample
-of the same workload, with every host core.
+of the same workload, with every host core busy.
 """
 from __future__ import annotations
 
@@ -157,18 +166,42 @@ def cpu_threads() -> int:
         return os.cpu_count() or 1
 
 
-def reference_sample(threads: int, n: int = 8192, workers: int = 8, heads: int = 1,
+def reference_sample(threads: int, n: int = 8192, workers: int = 8, heads: int | None = None,
                      schedule: str = "balanced") -> dict:
     """The reference CPU path (oracle/_ref/ref_driver: unmodified sources) on a
-    bounded sample of the workload: `heads` heads of seq n, P=workers threads
-    per head (concurrent executor), balanced forward + ring backward."""
+    bounded sample of the workload: `heads` heads of seq n run concurrently,
+    P=workers threads each (the reference's concurrent executor,
+    runtime.cpp:481-484), balanced forward + ring backward. By default
+    heads = threads // workers so every host core is busy; `threads` in the
+    result is the number of threads that actually ran."""
     from oracle import oracle as O
     if not O.ref_available():
         raise RuntimeError("oracle/_ref/ref_driver missing (build with `make -C oracle ref`)")
+    if heads is None:
+        heads = max(1, threads // workers)
     r = O.ref_time(n, workers, heads, D, schedule, threads)
     return {"seconds": r["seconds"], "tflops": r["tflops"], "threads": r["threads"],
-            "sample": f"{heads} head(s) x seq {n} x d {D}, P={workers} concurrent workers "
-                      f"({schedule} fwd + ring bwd), bf16-rounded fp64 inputs"}
+            "sample": f"{heads} head(s) x seq {n} x d {D} concurrently, P={workers} worker "
+                      f"threads each ({schedule} fwd + ring bwd, reference concurrent executor), "
+                      "bf16-rounded fp64 inputs"}
+
+
+def cpu_baseline(threads: int) -> dict:
+    """BASELINE.md's CPU anchors: the 16K sample (all cores) as the value,
+    BASELINE configs[0] (seq 4096, d=128, P=4, one head) timed in full beside
+    it. Larger configs are N^2 * H extrapolations of the anchor, labelled so."""
+    s = reference_sample(threads, n=16384, workers=8)
+    c1 = reference_sample(threads, n=4096, workers=4, heads=1)
+    per_head_s = s["seconds"] * (threads // 8 or 1) / max(1, s["threads"] // 8)
+    return {"value": s["tflops"], "unit": "TFLOP/s", "cores": s["threads"], "kind": "reference",
+            "sample": s["sample"], "seconds": s["seconds"],
+            "cfg1_seconds": c1["seconds"], "cfg1_threads": c1["threads"],
+            "cfg1": "BASELINE configs[0] in full: 1 head x seq 4096 x d 128, P=4 (balanced fwd + "
+                    "ring bwd), reference concurrent executor",
+            "cfg2_extrapolated_s": s["seconds"] * (32768 / 16384) ** 2 * 32 / max(1, s["threads"] // 8),
+            "extrapolation": "cfg2 (32 heads x 32K) from the 16K anchor by N^2 * H over the "
+                             "concurrently running heads (not measured)",
+            "per_head_s_16k": per_head_s}
 
 
 def run_reference(args):
@@ -186,16 +219,39 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": "attn fwd+bwd TFLOP/s", "value": v, "unit": "TFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": secs * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": secs * 1e3, "higher_is_better": True,
+        "scaling": "weak" if args.gpus == 1 else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "llama7b-attn causal fwd+bwd (reference CPU, bounded sample)",
-                   "heads": H, "d": D, "seq_len": SEQ},
+        "config": {"workload": "llama7b-attn causal fwd+bwd (reference CPU, bounded sample of "
+                               + _cfg(args)["name"] + ")",
+                   "heads": _cfg(args)["heads"], "d": D, "seq_len": _cfg(args)["seq"]},
         "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": vals[0]["threads"],
                          "kind": "reference", "sample": vals[0]["sample"]},
         "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+CONFIGS = {
+    # name: (total seq, q heads, kv heads, BASELINE configs[] index)
+    "cfg2": (32768, 32, 32, 1),
+    "cfg2gqa": (32768, 32, 8, 4),
+    "cfg3": (131072, 32, 32, 2),
+    "cfg4": (524288, 32, 32, 3),
+    "cfg5": (262144, 32, 8, 4),
+}
+
+
+def _cfg(args) -> dict:
+    name = args.config or ("cfg2" if args.gpus == 1 else "cfg3")
+    seq, hq, hkv, idx = CONFIGS[name]
+    if args.seq:
+        seq = args.seq
+    if args.heads:
+        hq = args.heads
+        hkv = min(hkv, hq) if hkv != CONFIGS[name][1] else hq
+    return {"name": name, "seq": seq, "heads": hq, "heads_kv": hkv, "baseline_index": idx}
 
 
 # ----------------------------------------------------------------------------- our arm, N=1
@@ -214,17 +270,17 @@ def run_single(args):
 
     dev = torch.device("cuda:0")
     torch.cuda.set_device(dev)
-    n = args.seq
-    heads = args.heads
+    cfg = _cfg(args)
+    n, heads, hkv = cfg["seq"], cfg["heads"], cfg["heads_kv"]
     stream = torch.cuda.current_stream()
 
     def rnd(*shape):
         return (torch.rand(*shape, device=dev) * 2 - 1).to(torch.bfloat16)
 
     torch.manual_seed(0)
-    q, k, v, d_out = rnd(heads, n, D), rnd(heads, n, D), rnd(heads, n, D), rnd(heads, n, D)
-    grads = F.ChunkGrads(torch.zeros(heads, n, D, device=dev), torch.empty(heads, n, D, device=dev),
-                         torch.empty(heads, n, D, device=dev))
+    q, k, v, d_out = rnd(heads, n, D), rnd(hkv, n, D), rnd(hkv, n, D), rnd(heads, n, D)
+    grads = F.ChunkGrads(torch.zeros(heads, n, D, device=dev), torch.empty(hkv, n, D, device=dev),
+                         torch.empty(hkv, n, D, device=dev))
 
     ev = {k_: [] for k_ in ("fwd", "aux", "bwd")}
     dflag = torch.zeros(1, dtype=torch.int32, device=dev)  # checked once after the timed loop
@@ -273,9 +329,10 @@ def run_single(args):
     # through the public host-buffer API (copies overlapped per head group)
     from paper_2310_03294_b200.pipeline import HostAttention
     hq, hk, hv, hdo = (t.cpu().pin_memory() for t in (q, k, v, d_out))
-    hdq, hdk, hdv = (torch.empty(heads, n, D, dtype=torch.bfloat16).pin_memory() for _ in range(3))
+    hdq, hdk, hdv = (torch.empty(*t.shape, dtype=torch.bfloat16).pin_memory() for t in (q, k, v))
     del grads
-    ha = HostAttention(heads, n, D, heads_per_group=args.heads_per_group, device=dev)
+    hpg = max(args.heads_per_group, heads // hkv)
+    ha = HostAttention(heads, n, D, heads_per_group=hpg, device=dev, heads_kv=hkv)
 
     def e2e_step():
         ha(hq, hk, hv, hdo, hdq, hdk, hdv, sync=False)
@@ -308,9 +365,11 @@ def run_single(args):
         "metric": "attn fwd+bwd TFLOP/s", "value": tflops, "unit": "TFLOP/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "llama7b-attn causal fwd+bwd, 32 heads, d=128, seq 32K, 1 B200 "
-                               "(BASELINE configs[1])",
-                   "heads": heads, "d": D, "seq_len": n, "mask": "causal", "workers": 1,
+        "config": {"workload": f"llama7b-attn causal fwd+bwd, {heads} q / {hkv} kv heads, d=128, "
+                               f"seq {n}, 1 B200 (BASELINE configs[{cfg['baseline_index']}]"
+                               + (" shape per GPU)" if cfg["name"] != "cfg2" else ")"),
+                   "name": cfg["name"], "heads": heads, "heads_kv": hkv, "d": D, "seq_len": n,
+                   "mask": "causal", "workers": 1,
                    "l2": "inputs (4 x %d MB) exceed L2; no flush" % (heads * n * D * 2 >> 20)},
         "tokens_per_s": n / (ms * 1e-3),
         "tflops_per_gpu": tflops,
@@ -321,24 +380,21 @@ def run_single(args):
         "roofline": {"bound": "tensor", "kernel": f"attn_{dom}_kernel", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "frac_of_sustained": achieved / peak_sus, "peak_source": src,
-                     "traffic": traffic,
+                     "traffic": traffic if cfg["name"] == "cfg2" else None,
                      "algorithmic_flops_per_launch": dom_flops},
         "e2e": {"value": fl / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
-                "path": "pipeline.HostAttention (flashcore.block_attn_update_final + backward_aux + "
-                        "block_attn_backward over the C ABI): pinned-host q/k/v/dO in, bf16 "
-                        "dQ/dK/dV out, copies overlapped per group of %d heads, 3 compute streams; consecutive "
-                        "steps overlap (step i+1's H2D of a group waits only for step i's compute of it)"
-                        % args.heads_per_group},
+                "path": "pipeline.HostAttention -> C++ host pipeline (da_pipeline_step: fwd with "
+                        "fused finalize + backward_aux + backward + bf16 conversion per head group): "
+                        "pinned-host q/k/v/dO in, bf16 dQ/dK/dV out, copies overlapped per group of "
+                        "%d heads, 3 compute streams; consecutive steps overlap (step i+1's H2D of a "
+                        "group waits only for step i's compute of it)" % hpg},
         "gpu_launches": 3 * args.steps,
         "clocks": clk.summary(),
     }
     if not args.no_cpu_baseline:
         try:
-            s = reference_sample(cpu_threads())
-            line["cpu_baseline"] = {"value": s["tflops"], "unit": "TFLOP/s", "cores": s["threads"],
-                                    "kind": "reference", "sample": s["sample"],
-                                    "seconds": s["seconds"]}
+            line["cpu_baseline"] = cpu_baseline(cpu_threads())
         except Exception as exc:  # pragma: no cover - reported, not fatal
             line["cpu_baseline"] = {"value": None, "unit": "TFLOP/s", "cores": cpu_threads(),
                                     "kind": "reference", "sample": f"unavailable: {exc}"}
@@ -346,36 +402,292 @@ def run_single(args):
     return 0
 
 
+# ----------------------------------------------------------------------------- our arm, N>1
+NVLINK_GBS = 770.0  # measured peer copy per direction per GPU (B200_PROFILING.md; 900 nominal)
+
+
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def spawn_ranks(args, argv) -> int:
+    """`python bench.py --gpus N` without torchrun: start the N ranks (one
+    process per GPU, rank 0 prints the line) and return the worst exit code."""
+    port = _free_port()
+    procs = []
+    for r in range(args.gpus):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(args.gpus),
+                   LOCAL_WORLD_SIZE=str(args.gpus), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, str(Path(__file__).resolve()), *argv],
+                                      env=env, stdout=None if r == 0 else subprocess.DEVNULL))
+    rcs = [None] * len(procs)
+    while any(rc is None for rc in rcs):
+        for i, p in enumerate(procs):
+            if rcs[i] is None:
+                rcs[i] = p.poll()
+        if any(rc not in (None, 0) for rc in rcs):  # one rank failed: the others would hang
+            for i, p in enumerate(procs):
+                if rcs[i] is None:
+                    p.kill()
+                    rcs[i] = p.wait()
+            break
+        time.sleep(0.2)
+    return max(abs(rc) for rc in rcs)
+
+
+def received_bytes(cf, cb, nq: int) -> int:
+    """Bytes this rank received in one fwd+bwd step, from the runtime's counters
+    (counted by the receiver, runtime.cpp:50-83 x heads): KV bf16, Q bf16,
+    forward partials fp32 (o | m | l), GradKV fp32, the backward (q, dO, lse,
+    D) bundle (q_scalars = nq * 258 -> nq * 520 bytes) and dq partials fp32."""
+    fwd = 2 * cf.kv_scalars + 2 * cf.q_scalars + 4 * cf.partial_scalars
+    bwd = 2 * cb.kv_scalars + 4 * cb.grad_scalars + 4 * cb.partial_scalars
+    bwd += cb.q_scalars * 520 // 258
+    return int(fwd + bwd)
+
+
 def run_multi(args):
-    from paper_2310_03294_b200 import dist
-    return dist.bench_main(args)
+    """One rank of the N-GPU run (torchrun or spawn_ranks): the native per-rank
+    runtime, device-timed legs, max over ranks, rank 0 prints the line."""
+    import torch
+    import torch.distributed as tdist
+    from paper_2310_03294_b200.rank import RankRuntime
+
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    if world != args.gpus:
+        raise SystemExit(f"WORLD_SIZE={world} but --gpus {args.gpus}")
+    ndev = torch.cuda.device_count()
+    if ndev < world and not args.share_gpu:
+        raise SystemExit(f"--gpus {world} needs {world} visible GPUs (found {ndev}); "
+                         "--share-gpu runs every rank on cuda:0 (tests)")
+    dev_index = 0 if args.share_gpu else local % ndev
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    # host bootstrap + timing reductions; the data plane is the runtime's own
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    transport = args.transport
+    if transport == "auto":
+        transport = "ipc" if args.share_gpu else "nccl"
+    cfg = _cfg(args)
+    seq, heads, hkv = cfg["seq"], cfg["heads"], cfg["heads_kv"]
+    if seq % world:
+        raise SystemExit(f"seq {seq} does not divide over {world} ranks")
+    rows = seq // world
+    torch.manual_seed(1234 + rank)
+
+    def rnd(h):
+        return (torch.rand(h, rows, D, device=dev) * 2 - 1).to(torch.bfloat16)
+
+    q, k, v, do = rnd(heads), rnd(hkv), rnd(hkv), rnd(heads)
+    runtimes = {}
+
+    def runtime(tr):
+        if tr not in runtimes:
+            runtimes[tr] = RankRuntime(rank, world, transport=tr,
+                                       nccl_max_ctas=args.nccl_max_ctas)
+        return runtimes[tr]
+
+    def timed(fwd, bwd, tr, steps, clk=None):
+        rt = runtime(tr)
+        res = {}
+
+        def step():
+            _, _, res["cf"] = rt.forward(q, k, v, fwd)
+            res["cb"] = rt.backward(do, bwd)[3]
+
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        tdist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if clk:
+            clk.timed(True)
+        s.record()
+        for _ in range(steps):
+            step()
+        e.record()
+        torch.cuda.synchronize()
+        if clk:
+            clk.timed(False)
+        tdist.barrier()
+        ms = torch.tensor([s.elapsed_time(e) / steps])
+        tdist.all_reduce(ms, op=tdist.ReduceOp.MAX)
+        return ms.item(), res["cf"], res["cb"]
+
+    fl = flops_fwd_bwd(seq, heads)
+    head_fwd, head_bwd = args.fwd_schedule, args.bwd_schedule
+    with ClockSampler(dev_index) as clk:  # started before the warm-up
+        ms, cf, cb = timed(head_fwd, head_bwd, transport, args.steps, clk)
+    legs = {f"{head_fwd}+{head_bwd}": {"ms": ms, "tflops": fl / (ms * 1e-3) / 1e12,
+                                       "transport": transport}}
+    if not args.no_legs:
+        leg_steps = max(2, args.leg_steps)
+        for name, f, b, tr in (("ring+ring", "ring", "ring", transport),
+                               ("balanced+balanced", "balanced", "balanced", transport),
+                               ("nocomm", head_fwd, head_bwd, "none")):
+            if name in legs:
+                continue
+            lms = timed(f, b, tr, leg_steps)[0]
+            legs[name] = {"ms": lms, "tflops": fl / (lms * 1e-3) / 1e12, "transport": tr,
+                          "fwd": f, "bwd": b}
+    nbytes = torch.tensor([float(received_bytes(cf, cb, heads * rows))])
+    tdist.all_reduce(nbytes, op=tdist.ReduceOp.MAX)
+    launches = torch.tensor([float(cf.attention_kernel_calls + cf.partial_messages + 1 + 1 +
+                                   cb.attention_kernel_calls + 2 * cb.grad_messages +
+                                   cb.partial_messages)])
+    tdist.all_reduce(launches, op=tdist.ReduceOp.SUM)
+
+    # e2e through the same public API with host buffers: each rank's shard is
+    # copied in from pinned host memory and its bf16 gradients out, inside the
+    # timed region; step j+1's copy-in and step j's copy-out overlap compute
+    rt = runtime(transport)
+    host_in = [t.cpu().pin_memory() for t in (q, k, v, do)]
+    host_out = [torch.empty(*t.shape, dtype=torch.bfloat16).pin_memory() for t in (q, k, v)]
+    dev_in = [[torch.empty_like(t) for t in (q, k, v, do)] for _ in range(2)]
+    cur = torch.cuda.current_stream()
+    h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    freed = [None, None]
+
+    def load(j):
+        slot = j % 2
+        with torch.cuda.stream(h2d):
+            if freed[slot] is not None:
+                h2d.wait_event(freed[slot])
+            for dst, src in zip(dev_in[slot], host_in):
+                dst.copy_(src, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(h2d)
+        return ev
+
+    def e2e_run(n_steps):
+        h2d.wait_stream(cur)
+        ready = load(0)
+        for j in range(n_steps):
+            nxt = load(j + 1) if j + 1 < n_steps else None  # prefetch
+            cur.wait_event(ready)
+            x = dev_in[j % 2]
+            rt.forward(x[0], x[1], x[2], head_fwd)
+            grads = rt.backward(x[3], head_bwd)[:3]
+            g16 = [g.to(torch.bfloat16) for g in grads]
+            done = torch.cuda.Event()
+            done.record(cur)
+            freed[j % 2] = done
+            d2h.wait_event(done)
+            with torch.cuda.stream(d2h):
+                for src, dst in zip(g16, host_out):
+                    dst.copy_(src, non_blocking=True)
+                    src.record_stream(d2h)
+            ready = nxt
+        cur.wait_stream(d2h)
+
+    e2e_run(2)
+    torch.cuda.synchronize()
+    tdist.barrier()
+    e_steps = max(2, args.steps)
+    s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s2.record()
+    e2e_run(e_steps)
+    e2.record()
+    torch.cuda.synchronize()
+    tdist.barrier()
+    ms_e2e = torch.tensor([s2.elapsed_time(e2) / e_steps])
+    tdist.all_reduce(ms_e2e, op=tdist.ReduceOp.MAX)
+    ms_e2e = ms_e2e.item()
+    for rt_ in runtimes.values():
+        rt_.close()
+
+    if rank == 0:
+        peak, peak_sus, src = peaks()
+        per_gpu = fl / (ms * 1e-3) / 1e12 / world
+        t_tensor = fl / world / (peak * 1e12)
+        t_link = nbytes.item() / (NVLINK_GBS * 1e9)
+        t_roof = max(t_tensor, t_link)
+        ring = legs.get("ring+ring", {}).get("ms")
+        nocomm = legs.get("nocomm", {}).get("ms")
+        line = {
+            "metric": "attn fwd+bwd TFLOP/s", "value": fl / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"llama7b-attn causal fwd+bwd, {heads} q / {hkv} kv heads, "
+                                   f"d=128, seq {seq} over {world} B200 (BASELINE configs"
+                                   f"[{cfg['baseline_index']}]), {head_fwd} fwd + {head_bwd} bwd, "
+                                   f"native per-rank runtime, {transport} transport",
+                       "name": cfg["name"], "heads": heads, "heads_kv": hkv, "d": D,
+                       "seq_len": seq, "tokens_per_gpu": rows, "fwd_schedule": head_fwd,
+                       "bwd_schedule": head_bwd, "transport": transport,
+                       "shared_gpu": bool(args.share_gpu),
+                       "l2": "inputs exceed L2; no flush"},
+            "tokens_per_s": seq / (ms * 1e-3),
+            "tflops_per_gpu": per_gpu,
+            "legs": legs,
+            "balanced_speedup_vs_ring": (ring / ms) if ring else None,
+            "exposed_comm_pct": (100.0 * (ms - nocomm) / nocomm) if nocomm else None,
+            "exposed_comm_definition": "(t - t_nocomm) / t_nocomm, t_nocomm = same kernels and "
+                                       "schedule on local buffers (analyzer.cpp:60-64)",
+            "roofline": {"bound": "tensor" if t_tensor >= t_link else "nvlink",
+                         "kernel": "whole step per GPU (compute + exposed NVLink)",
+                         "achieved": per_gpu, "peak": peak, "unit": "TFLOP/s",
+                         "frac": t_roof / (ms * 1e-3), "t_roof_ms": t_roof * 1e3,
+                         "t_tensor_ms": t_tensor * 1e3, "t_nvlink_ms": t_link * 1e3,
+                         "nvlink_bytes_per_gpu": nbytes.item(), "nvlink_gbs": NVLINK_GBS,
+                         "peak_source": src, "frac_of_sustained_tensor": per_gpu / peak_sus,
+                         "traffic": None},
+            "e2e": {"value": fl / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s",
+                    "h2d_bytes_per_step": sum(t.numel() * 2 for t in host_in) * world,
+                    "d2h_bytes_per_step": sum(t.numel() * 2 for t in host_out) * world,
+                    "ms_per_step": ms_e2e,
+                    "path": "rank.RankRuntime (C++ da_rank_*) forward/backward with pinned-host "
+                            "shards in and bf16 grads out, every rank; step j+1's copy-in and "
+                            "step j's copy-out overlap compute (two input sets, two copy streams)"},
+            "gpu_launches": int(launches.item()) * args.steps,
+            "clocks": clk.summary(),
+            "cpu_baseline_note": "the reference CPU path is timed at N=1 only (bench contract)",
+        }
+        print(json.dumps(line), flush=True)
+    tdist.destroy_process_group()
+    return 0
 
 
 def main(argv=None):
+    argv = list(sys.argv[1:] if argv is None else argv)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--seq", type=int, default=SEQ)
-    ap.add_argument("--heads", type=int, default=H)
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="default: cfg2 at N=1, cfg3 (128K over N) at N>1")
+    ap.add_argument("--seq", type=int, default=0, help="override the config's total tokens")
+    ap.add_argument("--heads", type=int, default=0, help="override the config's query heads")
     ap.add_argument("--heads-per-group", type=int, default=2)  # e2e copy/compute granularity (A/B: 2 >= 1 by ~0.5-1%)
-    ap.add_argument("--fwd-schedule", default="balanced", choices=["ring", "balanced", "balanced_split"])
+    ap.add_argument("--fwd-schedule", default="balanced_split",
+                    choices=["ring", "balanced", "balanced_split"])
     ap.add_argument("--bwd-schedule", default="balanced", choices=["ring", "balanced"])
-    ap.add_argument("--runtime", default="native", choices=["native", "python"],
-                    help="N>1: the C++ per-rank runtime (da_rank_*) or dist.DistRuntime")
-    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
-                    help="--runtime python: copy-engine pulls from peer HBM or NCCL send/recv")
+    ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "ipc"],
+                    help="N>1: NCCL send/recv (distinct GPUs) or CUDA-IPC pulls (shared GPU)")
+    ap.add_argument("--nccl-max-ctas", type=int, default=0)
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="N>1 on one GPU (every rank on cuda:0; tests the multi-rank path)")
+    ap.add_argument("--no-legs", action="store_true", help="N>1: headline leg only")
+    ap.add_argument("--leg-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--force-dist", action="store_true",
-                    help="run the torchrun/NCCL path even at one rank (tests the N>1 code)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    if args.gpus > 1 or world > 1 or args.force_dist:
+    if args.gpus > 1:
+        if "WORLD_SIZE" not in os.environ:
+            return spawn_ranks(args, argv)
         return run_multi(args)
     return run_single(args)
 

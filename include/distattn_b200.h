@@ -188,6 +188,34 @@ da_status da_host_dense_attention(const double* q, int64_t rows_q, const double*
                                   double scale, double* out, double* lse);
 
 /* ------------------------------------------------------------------------
+ * Host-buffer causal attention step with the PCIe copies overlapped per
+ * head group (C++ host layer; the reference's runtime takes host matrices,
+ * runtime.hpp:32-41, and prefetches the next operand during the current
+ * compute, runtime.cpp:280-284). One step = forward (fused finalize) +
+ * backward_aux + backward of a whole causal sequence on this GPU:
+ *   in:  pinned host bf16 q [heads, rows, 128], k / v [heads_kv, rows, 128], dO
+ *   out: pinned host bf16 dQ [heads, ...], dK / dV [heads_kv, ...]
+ * The saved O / LSE stay on the device (da_pipeline_outputs). Consecutive
+ * steps overlap (step i+1's copy-in of group g waits only for step i's
+ * compute of group g). sync != 0 joins onto `stream` and checks degenerate
+ * rows (DA_ERR_DEGENERATE_ROW); else call da_pipeline_join later.
+ * ------------------------------------------------------------------------ */
+typedef struct da_pipeline da_pipeline;
+da_status da_pipeline_create(int64_t heads, int64_t heads_kv, int64_t rows, int64_t d,
+                             int64_t heads_per_group, int compute_streams, da_pipeline** out);
+void da_pipeline_destroy(da_pipeline* p);
+da_status da_pipeline_step(da_pipeline* p, const void* hq, const void* hk, const void* hv,
+                           const void* hdo, void* hdq, void* hdk, void* hdv, int sync,
+                           void* stream);
+/* `stream` waits for every step issued so far; check_degenerate != 0 also
+ * reads the degenerate-row flag back (synchronises the stream). */
+da_status da_pipeline_join(da_pipeline* p, void* stream, int check_degenerate);
+/* Copies the last step's saved O (bf16 [heads, rows, 128]) and LSE (fp32
+ * [heads, rows]) into caller device buffers (either may be NULL), in order
+ * on `stream` after every step issued so far. */
+da_status da_pipeline_outputs(da_pipeline* p, void* out, float* lse, void* stream);
+
+/* ------------------------------------------------------------------------
  * Schedules (schedule.hpp:21-119, schedule.cpp:60-108).
  *
  * Flat, field-exact encoding of Schedule:

@@ -86,6 +86,11 @@ SIGNATURES = {
     "da_run_backward_sched": (C.c_int, [C.POINTER(Shards), C.c_int, C.POINTER(Counters), vp]),
     "da_run_backward": (C.c_int, [C.POINTER(Shards), C.POINTER(Counters), vp]),
     "da_runtime_release": (None, []),
+    "da_pipeline_create": (C.c_int, [i64, i64, i64, i64, i64, C.c_int, C.POINTER(vp)]),
+    "da_pipeline_destroy": (None, [vp]),
+    "da_pipeline_step": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, C.c_int, vp]),
+    "da_pipeline_join": (C.c_int, [vp, vp, C.c_int]),
+    "da_pipeline_outputs": (C.c_int, [vp, vp, vp, vp]),
     "da_run_forward_table": (C.c_int, [C.POINTER(Shards), i32, C.POINTER(i32), i64,
                                        C.POINTER(i32), i64, C.POINTER(Counters), vp]),
     "da_run_backward_table": (C.c_int, [C.POINTER(Shards), i32, C.POINTER(i32), i64,

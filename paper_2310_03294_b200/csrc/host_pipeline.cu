@@ -1,0 +1,299 @@
+// Host-buffer causal attention step (forward + backward over pinned host
+// tensors) with the PCIe transfers overlapped per head group — the C++ host
+// layer above the chunk kernels, the entry point bench.py's e2e leg and a
+// host-side caller use.
+//
+// The reference's public path takes host matrices (runtime.hpp:32-41) and
+// overlaps the next chunk's transfer with the current chunk's compute
+// (prefetch depth 1, runtime.cpp:280-284, 427-431). Here the same idea is
+// applied to the host<->HBM copies of one full causal forward + backward:
+// the query heads are split into groups (aligned to whole GQA kv groups);
+// while group g computes (forward with fused finalize, backward preprocess,
+// backward, fp32->bf16 conversion of dQ/dK/dV), group g+1's q/k/v/dO are in
+// flight host->device on one copy stream and group g-1's gradients
+// device->host on another. Groups rotate over several compute streams so
+// one group's backward tail overlaps the next group's forward. Heads are
+// independent, so grouping changes no arithmetic.
+//
+// Consecutive calls pipeline too: call i+1's copy-in of group g waits only
+// for call i's compute of group g, and its compute for call i's copy-out of
+// group g. Degenerate rows set one device flag, checked on join (sync) — the
+// reference's DegenerateRowError (flashcore.hpp:233-235) without a sync per
+// group.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <vector>
+
+#include "capi_internal.h"
+#include "kernels.h"
+
+struct da_pipeline {
+  int64_t heads = 0, heads_kv = 0, rows = 0, hg = 0, groups = 0;
+  // device tensors
+  void *q = nullptr, *k = nullptr, *v = nullptr, *d_out = nullptr, *out = nullptr;
+  float *lse = nullptr, *dvec = nullptr, *dq = nullptr, *dk = nullptr, *dv = nullptr;
+  void *dq16 = nullptr, *dk16 = nullptr, *dv16 = nullptr;
+  int* flag = nullptr;
+  bool flag_clear = true;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  std::vector<cudaStream_t> comp;
+  cudaEvent_t start = nullptr;
+  std::vector<cudaEvent_t> fwd_ready, in_ready, comp_done[2], d2h_done[2];
+  int parity = 0;      // which comp_done / d2h_done set the next call records
+  bool has_prev = false;
+  std::vector<void*> allocs;
+};
+
+namespace da {
+namespace {
+
+da_status ck(cudaError_t e, const char* where) {
+  return e == cudaSuccess ? DA_OK : cuda_error(e, where);
+}
+
+#define P_TRY(x)                 \
+  do {                           \
+    const da_status s_ = (x);    \
+    if (s_ != DA_OK) return s_;  \
+  } while (0)
+
+void release(da_pipeline* p) {
+  if (p == nullptr) return;
+  cudaDeviceSynchronize();
+  for (void* a : p->allocs) cudaFree(a);
+  auto ev = [](std::vector<cudaEvent_t>& v) {
+    for (cudaEvent_t e : v)
+      if (e) cudaEventDestroy(e);
+  };
+  ev(p->fwd_ready);
+  ev(p->in_ready);
+  for (int i = 0; i < 2; ++i) {
+    ev(p->comp_done[i]);
+    ev(p->d2h_done[i]);
+  }
+  if (p->start) cudaEventDestroy(p->start);
+  for (cudaStream_t s : p->comp)
+    if (s) cudaStreamDestroy(s);
+  if (p->h2d) cudaStreamDestroy(p->h2d);
+  if (p->d2h) cudaStreamDestroy(p->d2h);
+  delete p;
+}
+
+}  // namespace
+}  // namespace da
+
+using namespace da;
+
+extern "C" {
+
+da_status da_pipeline_create(int64_t heads, int64_t heads_kv, int64_t rows, int64_t d,
+                             int64_t heads_per_group, int compute_streams, da_pipeline** out) {
+  if (out == nullptr) return set_error(DA_ERR_CONFIG, "da_pipeline_create: null output");
+  if (d != 128) return set_error(DA_ERR_UNSUPPORTED, "da_pipeline_create: d must be 128");
+  if (heads < 1 || heads_kv < 1 || heads % heads_kv != 0 || rows < 1)
+    return set_error(DA_ERR_SHAPE, "da_pipeline_create: heads must be a multiple of heads_kv");
+  const int64_t ratio = heads / heads_kv;
+  if (heads_per_group < 1 || heads % heads_per_group != 0 || heads_per_group % ratio != 0)
+    return set_error(DA_ERR_SHAPE,
+                     "da_pipeline_create: heads_per_group must divide heads and cover whole "
+                     "kv groups");
+  da_pipeline* p = new da_pipeline();
+  p->heads = heads;
+  p->heads_kv = heads_kv;
+  p->rows = rows;
+  p->hg = heads_per_group;
+  p->groups = heads / heads_per_group;
+  const size_t nq = static_cast<size_t>(heads) * rows, nkv = static_cast<size_t>(heads_kv) * rows;
+  auto get = [&](size_t bytes, void** dst) -> da_status {
+    const cudaError_t e = cudaMalloc(dst, bytes);
+    if (e != cudaSuccess) return cuda_error(e, "da_pipeline_create alloc");
+    p->allocs.push_back(*dst);
+    return DA_OK;
+  };
+  da_status s = DA_OK;
+  void* t = nullptr;
+  auto fail = [&](da_status st) {
+    release(p);
+    return st;
+  };
+  if ((s = get(nq * 256, &p->q)) != DA_OK) return fail(s);
+  if ((s = get(nkv * 256, &p->k)) != DA_OK) return fail(s);
+  if ((s = get(nkv * 256, &p->v)) != DA_OK) return fail(s);
+  if ((s = get(nq * 256, &p->d_out)) != DA_OK) return fail(s);
+  if ((s = get(nq * 256, &p->out)) != DA_OK) return fail(s);
+  if ((s = get(nq * 4, &t)) != DA_OK) return fail(s);
+  p->lse = static_cast<float*>(t);
+  if ((s = get(nq * 4, &t)) != DA_OK) return fail(s);
+  p->dvec = static_cast<float*>(t);
+  if ((s = get(nq * 512, &t)) != DA_OK) return fail(s);
+  p->dq = static_cast<float*>(t);
+  if ((s = get(nkv * 512, &t)) != DA_OK) return fail(s);
+  p->dk = static_cast<float*>(t);
+  if ((s = get(nkv * 512, &t)) != DA_OK) return fail(s);
+  p->dv = static_cast<float*>(t);
+  if ((s = get(nq * 256, &p->dq16)) != DA_OK) return fail(s);
+  if ((s = get(nkv * 256, &p->dk16)) != DA_OK) return fail(s);
+  if ((s = get(nkv * 256, &p->dv16)) != DA_OK) return fail(s);
+  if ((s = get(sizeof(int), &t)) != DA_OK) return fail(s);
+  p->flag = static_cast<int*>(t);
+  if ((s = ck(cudaMemset(p->flag, 0, sizeof(int)), "flag")) != DA_OK) return fail(s);
+  if ((s = ck(cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking), "stream")) != DA_OK)
+    return fail(s);
+  if ((s = ck(cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking), "stream")) != DA_OK)
+    return fail(s);
+  p->comp.assign(compute_streams < 1 ? 1 : compute_streams, nullptr);
+  for (auto& c : p->comp)
+    if ((s = ck(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking), "stream")) != DA_OK)
+      return fail(s);
+  auto mk = [&](std::vector<cudaEvent_t>& v) -> da_status {
+    v.assign(p->groups, nullptr);
+    for (auto& e : v) P_TRY(ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event"));
+    return DA_OK;
+  };
+  if ((s = mk(p->fwd_ready)) != DA_OK || (s = mk(p->in_ready)) != DA_OK) return fail(s);
+  for (int i = 0; i < 2; ++i)
+    if ((s = mk(p->comp_done[i])) != DA_OK || (s = mk(p->d2h_done[i])) != DA_OK) return fail(s);
+  if ((s = ck(cudaEventCreateWithFlags(&p->start, cudaEventDisableTiming), "event")) != DA_OK)
+    return fail(s);
+  *out = p;
+  return DA_OK;
+}
+
+void da_pipeline_destroy(da_pipeline* p) { release(p); }
+
+da_status da_pipeline_step(da_pipeline* p, const void* hq, const void* hk, const void* hv,
+                           const void* hdo, void* hdq, void* hdk, void* hdv, int sync,
+                           void* stream) {
+  if (p == nullptr) return set_error(DA_ERR_CONFIG, "da_pipeline_step: null pipeline");
+  if (!hq || !hk || !hv || !hdo || !hdq || !hdk || !hdv)
+    return set_error(DA_ERR_CONFIG, "da_pipeline_step: null host buffer");
+  cudaStream_t cur = reinterpret_cast<cudaStream_t>(stream);
+  if (p->flag_clear) {  // an unchecked (sync = 0) call's flag stays sticky until checked
+    P_TRY(ck(cudaMemsetAsync(p->flag, 0, sizeof(int), cur), "flag"));
+    p->flag_clear = false;
+  }
+  const int64_t ratio = p->heads / p->heads_kv, hgk = p->hg / ratio;
+  const size_t qb = static_cast<size_t>(p->hg) * p->rows * 256;  // bytes of a group's q slice
+  const size_t kb = static_cast<size_t>(hgk) * p->rows * 256;
+  const int cs = p->parity, ps = 1 - p->parity;
+  // the caller's preceding work (and its timing events) comes first
+  P_TRY(ck(cudaEventRecord(p->start, cur), "event"));
+  P_TRY(ck(cudaStreamWaitEvent(p->h2d, p->start, 0), "wait"));
+  for (cudaStream_t c : p->comp) P_TRY(ck(cudaStreamWaitEvent(c, p->start, 0), "wait"));
+  auto off = [](const void* base, size_t bytes) {
+    return static_cast<char*>(const_cast<void*>(base)) + bytes;
+  };
+  for (int64_t g = 0; g < p->groups; ++g) {
+    if (p->has_prev)  // the previous call's readers of these slices
+      P_TRY(ck(cudaStreamWaitEvent(p->h2d, p->comp_done[ps][g], 0), "wait"));
+    P_TRY(ck(cudaMemcpyAsync(off(p->q, g * qb), off(hq, g * qb), qb, cudaMemcpyHostToDevice,
+                             p->h2d), "h2d q"));
+    P_TRY(ck(cudaMemcpyAsync(off(p->k, g * kb), off(hk, g * kb), kb, cudaMemcpyHostToDevice,
+                             p->h2d), "h2d k"));
+    P_TRY(ck(cudaMemcpyAsync(off(p->v, g * kb), off(hv, g * kb), kb, cudaMemcpyHostToDevice,
+                             p->h2d), "h2d v"));
+    P_TRY(ck(cudaEventRecord(p->fwd_ready[g], p->h2d), "event"));
+    // dO is first needed by the backward: its copy overlaps the forward
+    P_TRY(ck(cudaMemcpyAsync(off(p->d_out, g * qb), off(hdo, g * qb), qb,
+                             cudaMemcpyHostToDevice, p->h2d), "h2d dO"));
+    P_TRY(ck(cudaEventRecord(p->in_ready[g], p->h2d), "event"));
+  }
+  const int64_t qr = p->hg * p->rows, kr = hgk * p->rows;  // rows of a group
+  for (int64_t g = 0; g < p->groups; ++g) {
+    cudaStream_t c = p->comp[g % p->comp.size()];
+    P_TRY(ck(cudaStreamWaitEvent(c, p->fwd_ready[g], 0), "wait"));
+    if (p->has_prev)  // the previous call's copy-out of this group's gradients
+      P_TRY(ck(cudaStreamWaitEvent(c, p->d2h_done[ps][g], 0), "wait"));
+    void* q = off(p->q, g * qb);
+    void* k = off(p->k, g * kb);
+    void* v = off(p->v, g * kb);
+    void* o = off(p->out, g * qb);
+    void* d_out = off(p->d_out, g * qb);
+    float* lse = p->lse + g * qr;
+    float* dvec = p->dvec + g * qr;
+    float* dq = p->dq + g * qr * 128;
+    float* dk = p->dk + g * kr * 128;
+    float* dv = p->dv + g * kr * 128;
+    da_fwd_args a{};
+    a.q = q;
+    a.k = k;
+    a.v = v;
+    a.h_q = p->hg;
+    a.h_kv = hgk;
+    a.rows_q = a.rows_kv = p->rows;
+    a.d = 128;
+    a.o_out = o;
+    a.lse_out = lse;
+    a.degenerate_flag = p->flag;
+    a.mask = DA_MASK_DIAGONAL;
+    a.finalize = 1;
+    P_TRY(da_attn_fwd_chunk(&a, c));
+    P_TRY(ck(cudaStreamWaitEvent(c, p->in_ready[g], 0), "wait"));
+    P_TRY(ck(launch_bwd_preprocess(d_out, o, dvec, qr, c), "preprocess"));
+    P_TRY(ck(cudaMemsetAsync(dq, 0, static_cast<size_t>(qr) * 512, c), "dq zero"));
+    da_bwd_args b{};
+    b.q = q;
+    b.k = k;
+    b.v = v;
+    b.d_out = d_out;
+    b.lse = lse;
+    b.d_vec = dvec;
+    b.h_q = p->hg;
+    b.h_kv = hgk;
+    b.rows_q = b.rows_kv = p->rows;
+    b.d = 128;
+    b.dq_acc = dq;
+    b.dk_acc = dk;
+    b.dv_acc = dv;
+    b.mask = DA_MASK_DIAGONAL;
+    P_TRY(da_attn_bwd_chunk(&b, c));
+    P_TRY(ck(launch_convert(dq, off(p->dq16, g * qb), qr * 128, c), "convert"));
+    P_TRY(ck(launch_convert(dk, off(p->dk16, g * kb), kr * 128, c), "convert"));
+    P_TRY(ck(launch_convert(dv, off(p->dv16, g * kb), kr * 128, c), "convert"));
+    P_TRY(ck(cudaEventRecord(p->comp_done[cs][g], c), "event"));
+    P_TRY(ck(cudaStreamWaitEvent(p->d2h, p->comp_done[cs][g], 0), "wait"));
+    P_TRY(ck(cudaMemcpyAsync(off(hdq, g * qb), off(p->dq16, g * qb), qb, cudaMemcpyDeviceToHost,
+                             p->d2h), "d2h dq"));
+    P_TRY(ck(cudaMemcpyAsync(off(hdk, g * kb), off(p->dk16, g * kb), kb, cudaMemcpyDeviceToHost,
+                             p->d2h), "d2h dk"));
+    P_TRY(ck(cudaMemcpyAsync(off(hdv, g * kb), off(p->dv16, g * kb), kb, cudaMemcpyDeviceToHost,
+                             p->d2h), "d2h dv"));
+    P_TRY(ck(cudaEventRecord(p->d2h_done[cs][g], p->d2h), "event"));
+  }
+  p->parity = ps;
+  p->has_prev = true;
+  if (sync) return da_pipeline_join(p, stream, 1);
+  return DA_OK;
+}
+
+da_status da_pipeline_join(da_pipeline* p, void* stream, int check_degenerate) {
+  if (p == nullptr) return set_error(DA_ERR_CONFIG, "da_pipeline_join: null pipeline");
+  cudaStream_t cur = reinterpret_cast<cudaStream_t>(stream);
+  cudaEvent_t e;
+  P_TRY(ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event"));
+  for (cudaStream_t s : {p->d2h, p->h2d}) {
+    P_TRY(ck(cudaEventRecord(e, s), "event"));
+    P_TRY(ck(cudaStreamWaitEvent(cur, e, 0), "wait"));
+  }
+  for (cudaStream_t s : p->comp) {
+    P_TRY(ck(cudaEventRecord(e, s), "event"));
+    P_TRY(ck(cudaStreamWaitEvent(cur, e, 0), "wait"));
+  }
+  cudaEventDestroy(e);
+  if (!check_degenerate) return DA_OK;
+  p->flag_clear = true;
+  return da_check_degenerate(p->flag, stream);
+}
+
+da_status da_pipeline_outputs(da_pipeline* p, void* out, float* lse, void* stream) {
+  if (p == nullptr) return set_error(DA_ERR_CONFIG, "da_pipeline_outputs: null pipeline");
+  cudaStream_t cur = reinterpret_cast<cudaStream_t>(stream);
+  P_TRY(da_pipeline_join(p, stream, 0));
+  const size_t nq = static_cast<size_t>(p->heads) * p->rows;
+  if (out) P_TRY(ck(cudaMemcpyAsync(out, p->out, nq * 256, cudaMemcpyDeviceToDevice, cur), "O"));
+  if (lse) P_TRY(ck(cudaMemcpyAsync(lse, p->lse, nq * 4, cudaMemcpyDeviceToDevice, cur), "LSE"));
+  return DA_OK;
+}
+
+}  // extern "C"

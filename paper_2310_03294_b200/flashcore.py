@@ -227,7 +227,10 @@ def block_attn_backward(q, k, v, out, lse, d_out, mask: MaskMode, scale: float |
     _req(lse, torch.float32, "lse")
     h_q, rows_q, d = q.shape
     h_kv, rows_kv, _ = k.shape
-    if tuple(out.shape) != (h_q, rows_q, d):
+    if out is None and d_vec is None:
+        from .errors import StateError
+        raise StateError("block_attn_backward: needs the forward output (or its D = backward_aux)")
+    if out is not None and tuple(out.shape) != (h_q, rows_q, d):
         _shape_error("block_attn_backward: output shape mismatch")
     if tuple(d_out.shape) != (h_q, rows_q, d):
         _shape_error("block_attn_backward: upstream grad shape mismatch")

@@ -170,7 +170,8 @@ def test_peaky_fwd_bwd_chunk_chain(cuda, amp):
 
 @pytest.mark.parametrize("h,n,hpg", [(4, 1024, 2), (6, 700, 3), (2, 256, 2)])
 def test_host_pipeline_matches_direct_calls(cuda, h, n, hpg):
-    """pipeline.HostAttention (pinned host in/out, per-head-group overlap) computes
+    """pipeline.HostAttention (the C++ host pipeline, da_pipeline_*: pinned host
+    in/out, per-head-group overlap) computes
     the same step as the ungrouped device calls: dK/dV bit-exact (deterministic
     in-CTA reductions), dQ within one bf16 ulp (fp32 reduction order differs)."""
     from paper_2310_03294_b200 import flashcore as F
@@ -188,7 +189,7 @@ def test_host_pipeline_matches_direct_calls(cuda, h, n, hpg):
     assert torch.equal(host_out[1], ref[1]) and torch.equal(host_out[2], ref[2])
     assert rel_err(host_out[0].float(), ref[0].float()) < 1e-2
     o_ref, _ = attention_ref(q, k, v, True)
-    assert rel_err(torch.cat(ha.out, 0), o_ref) < TOL
+    assert rel_err(ha.outputs()[0], o_ref) < TOL
 
 
 def test_host_pipeline_back_to_back_async_calls(cuda):
@@ -306,3 +307,24 @@ def test_deterministic_backward_on_two_streams(cuda):
     torch.cuda.synchronize()
     for g in res[1:]:
         assert torch.equal(g.dq, res[0].dq) and torch.equal(g.dk, res[0].dk)
+
+
+def test_host_pipeline_gqa(cuda):
+    """The C++ host pipeline with GQA (8 q heads / 2 kv heads, groups of one kv
+    group): dK/dV summed over each group, equal to the device calls."""
+    from paper_2310_03294_b200 import flashcore as F
+    from paper_2310_03294_b200.pipeline import HostAttention
+    h, hk, n = 8, 2, 640
+    q, k, v = _qkv(h, n, hk, seed=77)
+    do = _qkv(h, n, seed=78)[0]
+    out = F.block_attn_update_final(q, k, v, None, F.MaskMode.Diagonal)
+    g = F.block_attn_backward(q, k, v, out.o, out.lse, do, F.MaskMode.Diagonal)
+    host_in = [x.cpu().pin_memory() for x in (q, k, v, do)]
+    host_out = [torch.empty(*x.shape, dtype=torch.bfloat16).pin_memory() for x in (q, k, v)]
+    ha = HostAttention(h, n, heads_per_group=4, heads_kv=hk)
+    ha(*host_in, *host_out)
+    assert torch.equal(host_out[1], g.dk.to(torch.bfloat16).cpu())
+    assert torch.equal(host_out[2], g.dv.to(torch.bfloat16).cpu())
+    assert rel_err(host_out[0].float(), g.dq.to(torch.bfloat16).cpu().float()) < 1e-2
+    with pytest.raises(Exception):
+        HostAttention(h, n, heads_per_group=2, heads_kv=hk)  # splits a kv group

@@ -114,7 +114,7 @@ def test_native_rank_runtime(cuda, world, n, heads, fwd, bwd, heads_kv):
 def test_native_rank_runtime_deterministic_backward(cuda, world, fwd, bwd):
     """deterministic=True: the distributed backward repeats bit for bit (the
     reference's executors do, runtime.hpp:7-9) and still matches the oracle."""
-    n, heads = 1024, 2
+    n, heads = 256 * world, 2
     with tempfile.TemporaryDirectory() as td:
         mp.spawn(_worker, args=(world, _port(), n, heads, fwd, bwd, td, None, "ipc", True),
                  nprocs=world, join=True)
