@@ -116,5 +116,10 @@ class RankRuntime:
 
 
 def _counters(c) -> CommCounters:
-    return CommCounters(c.kv_scalars, c.q_scalars, c.partial_scalars, c.grad_scalars,
-                        c.kv_messages, c.q_messages, c.partial_messages, c.grad_messages)
+    """The reference's CommCounters (runtime.hpp:49-63) plus the trace's kernel
+    call count and residency high-water mark (ExecutionTrace, runtime.hpp:83-91)."""
+    cc = CommCounters(c.kv_scalars, c.q_scalars, c.partial_scalars, c.grad_scalars,
+                      c.kv_messages, c.q_messages, c.partial_messages, c.grad_messages)
+    cc.attention_kernel_calls = c.attention_kernel_calls
+    cc.max_remote_chunks_held = c.max_remote_chunks_held
+    return cc
