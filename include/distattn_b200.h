@@ -378,6 +378,12 @@ da_status da_rank_forward(da_rank* r, int schedule_kind, const void* q, const vo
                           float* lse, da_counters* counters, void* stream);
 da_status da_rank_backward(da_rank* r, int schedule_kind, const void* d_out, float* dq, float* dk,
                            float* dv, da_counters* counters, void* stream);
+/* Re-installs a saved forward state (this rank's q, k, v, O, LSE of an
+ * earlier pass) for the next da_rank_backward — the rematerialisation hook
+ * of a checkpointed multi-layer model (ckptplan.cpp:198-206): each layer's
+ * attention backward uses its own saved O / LSE, never a recompute. */
+da_status da_rank_restore(da_rank* r, const void* q, const void* k, const void* v, void* out,
+                          float* lse, int64_t h_q, int64_t h_kv, int64_t rows);
 /* The message protocol of one rank without a device: 5 int32 per entry
  * {pass (0 forward, 1 backward), phase (2t = operands(t), 2t+1 = results(t)),
  * dir (0 send, 1 receive), peer rank, buffer key}; *n = entries (written up to

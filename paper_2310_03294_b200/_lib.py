@@ -63,6 +63,7 @@ SIGNATURES = {
     "da_stream_write_u32": (C.c_int, [vp, vp, C.c_uint32]),
     "da_rank_create": (C.c_int, [C.c_int, C.c_int, vp, vp, C.POINTER(vp)]),
     "da_rank_destroy": (None, [vp]),
+    "da_rank_restore": (C.c_int, [vp, vp, vp, vp, vp, vp, i64, i64, i64]),
     "da_rank_create_ex": (C.c_int, [C.c_int, C.c_int, vp, vp, vp, C.POINTER(vp)]),
     "da_rank_protocol": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(i32), i64,
                                    C.POINTER(i64)]),

@@ -227,9 +227,50 @@ def _tokens(x: torch.Tensor) -> torch.Tensor:
     return x.permute(1, 0, 2).reshape(n, h * HEAD_DIM).float()
 
 
+class LocalAttention:
+    """The layer's attention op on ONE device: the chunk kernels over the whole
+    local sequence (Diagonal mask, fused finalize; deterministic dQ)."""
+
+    def forward(self, q, k, v, scale):
+        o = F.block_attn_update_final(q, k, v, None, F.MaskMode.Diagonal, scale)
+        return o.o, o.lse
+
+    def backward(self, q, k, v, o, lse, d_out, scale):
+        g = F.block_attn_backward(q, k, v, o, lse, d_out, F.MaskMode.Diagonal, scale,
+                                  deterministic=True)
+        return g.dq, g.dk, g.dv
+
+
+class SeqParallelAttention:
+    """The layer's attention op as DistFlashAttn: the sequence is sharded over
+    the ranks of a rank.RankRuntime (one process per GPU), each rank holding
+    its contiguous token chunk of every activation; attention runs the
+    schedule-driven distributed forward / backward. The
+    backward re-installs the layer's saved (q, k, v, O, LSE) — under
+    AttentionOutput those are the checkpointed forward outputs, so the
+    attention forward is never recomputed (ckptplan.cpp:146-155, 198-206).
+    The runtime must be created with deterministic=True for the reference's
+    bitwise cross-plan property (ckptplan.hpp:8-9). Every call is collective:
+    all ranks run the same plan, so the calls line up."""
+
+    def __init__(self, runtime, fwd_schedule: str = "balanced", bwd_schedule: str = "balanced"):
+        self.rt, self.fwd_schedule, self.bwd_schedule = runtime, fwd_schedule, bwd_schedule
+
+    def forward(self, q, k, v, scale):
+        if abs(scale - 1.0 / math.sqrt(HEAD_DIM)) > 1e-12:
+            raise ConfigError("the per-rank runtime uses scale 1/sqrt(128)")
+        out, lse, _ = self.rt.forward(q, k, v, self.fwd_schedule)
+        return out, lse
+
+    def backward(self, q, k, v, o, lse, d_out, scale):
+        dq, dk, dv, _ = self.rt.backward(d_out, self.bwd_schedule, saved=(q, k, v, o, lse))
+        return dq, dk, dv
+
+
 class _Exec:
-    def __init__(self, pipe: LayerPipeline):
+    def __init__(self, pipe: LayerPipeline, attention=None):
         self.pipe = pipe
+        self.attention = attention if attention is not None else LocalAttention()
         self.fwd_launches = 0
         self.bwd_launches = 0
 
@@ -245,10 +286,10 @@ class _Exec:
             out.a, out.b, out.c = _mm(v.a, lw.wq), _mm(v.a, lw.wk), _mm(v.a, lw.wv)
         elif k == OpKind.Attention:
             h = pipe.heads
-            o = F.block_attn_update_final(_heads(v.a, h), _heads(v.b, h), _heads(v.c, h), None,
-                                          F.MaskMode.Diagonal, pipe.scale)
+            o, lse = self.attention.forward(_heads(v.a, h), _heads(v.b, h), _heads(v.c, h),
+                                            pipe.scale)
             self.fwd_launches += 1
-            out.a, out.stat = _tokens(o.o), o.lse
+            out.a, out.stat = _tokens(o), lse
         elif k == OpKind.OutProj:
             out.a = _mm(v.a, lw.wo)
         elif k == OpKind.MlpUp:
@@ -276,11 +317,11 @@ class _Exec:
             # consumes the op's OUTPUT value (O, logsumexp): saved under
             # AttentionOutput, recomputed under LayerBoundary
             h = pipe.heads
-            gr = F.block_attn_backward(_heads(vin.a, h), _heads(vin.b, h), _heads(vin.c, h),
-                                       _heads(vout.a, h), vout.stat, _heads(g.a, h),
-                                       F.MaskMode.Diagonal, pipe.scale, deterministic=True)
+            dq, dk, dv = self.attention.backward(_heads(vin.a, h), _heads(vin.b, h),
+                                                 _heads(vin.c, h), _heads(vout.a, h), vout.stat,
+                                                 _heads(g.a, h), pipe.scale)
             self.bwd_launches += 1
-            dx.a, dx.b, dx.c = _tokens(gr.dq), _tokens(gr.dk), _tokens(gr.dv)
+            dx.a, dx.b, dx.c = _tokens(dq), _tokens(dk), _tokens(dv)
         elif k == OpKind.OutProj:
             lg.dwo = _wgrad(vin.a, g.a)
             dx.a = _mm_t(g.a, lw.wo)
@@ -297,12 +338,15 @@ class _Exec:
 
 
 def run_with_checkpointing(pipe: LayerPipeline, p: CheckpointPlan, x: torch.Tensor,
-                           d_out: torch.Tensor, executor=None) -> CkptRunResult:
+                           d_out: torch.Tensor, executor=None, attention=None) -> CkptRunResult:
     """ckptplan.cpp:236-305: forward keeping only the plan's values, then the
     backward segment by segment, recomputing each from its checkpoint; a
     segment-final attention whose output was saved (AttentionOutput) is not
     recomputed. `executor` (forward/backward per op) defaults to the device
-    ops; tests substitute a recording stub to check the control flow on CPU."""
+    ops; tests substitute a recording stub to check the control flow on CPU.
+    `attention`: LocalAttention (default) or SeqParallelAttention — then x /
+    d_out are this rank's token shard and pipe.tokens the shard's rows, and
+    the weight gradients are this rank's partial sums (all-reduce them)."""
     if not pipe.layers:
         raise ConfigError("pipeline needs at least 1 layer")
     if tuple(x.shape) != (pipe.tokens, pipe.d):
@@ -317,7 +361,7 @@ def run_with_checkpointing(pipe: LayerPipeline, p: CheckpointPlan, x: torch.Tens
         if pos < 0 or pos > n_ops:
             raise ConfigError("saved position out of range")
         saved[pos] = True
-    ex = executor if executor is not None else _Exec(pipe)
+    ex = executor if executor is not None else _Exec(pipe, attention)
     store: dict[int, _Value] = {0: _Value(a=x.float())}
     cur = store[0]
     for op in range(n_ops):

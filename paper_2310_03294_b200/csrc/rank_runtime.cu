@@ -911,6 +911,29 @@ da_status da_rank_backward(da_rank* r, int schedule_kind, const void* d_out, flo
   return DA_OK;
 }
 
+// Re-installs a saved forward state (q, k, v, O, LSE of an earlier forward
+// pass) for the next da_rank_backward: the rematerialisation hook of a
+// checkpointed multi-layer model (ckptplan.cpp:198-206), whose attention
+// backward runs with the saved O / LSE of ITS layer, never a recompute.
+da_status da_rank_restore(da_rank* r, const void* q, const void* k, const void* v, void* out,
+                          float* lse, int64_t h_q, int64_t h_kv, int64_t rows) {
+  if (r == nullptr) return set_error(DA_ERR_CONFIG, "da_rank_restore: null runtime");
+  if (!q || !k || !v || !out || !lse)
+    return set_error(DA_ERR_STATE, "run_backward requires forward output and logsumexp");
+  if (h_q < 1 || h_kv < 1 || h_q % h_kv != 0 || rows < 1)
+    return set_error(DA_ERR_SHAPE, "da_rank_restore: bad shape");
+  r->q = q;
+  r->k = k;
+  r->v = v;
+  r->out = out;
+  r->lse = lse;
+  r->h_q = h_q;
+  r->h_kv = h_kv;
+  r->rows = rows;
+  r->have_forward = true;
+  return DA_OK;
+}
+
 // The pass's phase lists of one rank, without a device (protocol tests):
 // per entry {pass (0 fwd, 1 bwd), phase (2t + 0 operands(t), 2t + 1
 // results(t)), dir (0 send, 1 recv), peer (0-based), key}.

@@ -81,9 +81,27 @@ class RankRuntime:
         self._saved = (q, k, v, out, lse)  # the runtime holds pointers to these
         return out, lse, _counters(c)
 
-    def backward(self, d_out: torch.Tensor, schedule: str = "ring", stream=None):
+    def backward(self, d_out: torch.Tensor, schedule: str = "ring", stream=None, saved=None):
+        """run_backward of this rank. `saved` = (q, k, v, out, lse) of an earlier
+        forward re-installs that pass's state (a checkpointed multi-layer
+        model: each layer's backward uses its own saved O / LSE); default: the
+        last forward."""
         from .errors import ConfigError, ShapeError, StateError
         from .flashcore import _req
+        if saved is not None:
+            q, k, v, out, lse = saved
+            if out is None or lse is None:
+                raise StateError("run_backward requires forward output and logsumexp")
+            for t, n in ((q, "q"), (k, "k"), (v, "v"), (out, "out")):
+                _req(t, torch.bfloat16, n)
+            _req(lse, torch.float32, "lse")
+            if out.shape != q.shape or tuple(lse.shape) != tuple(q.shape[:2]) or \
+                    k.shape != v.shape or k.shape[1] != q.shape[1]:
+                raise ShapeError("run_backward: saved state shapes disagree")
+            check(_lib.lib().da_rank_restore(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                             out.data_ptr(), lse.data_ptr(), q.shape[0],
+                                             k.shape[0], q.shape[1]))
+            self._saved = (q, k, v, out, lse)
         q, k, v, out, lse = self._saved if self._saved else (None,) * 5
         if q is None:
             raise StateError("run_backward requires forward output and logsumexp")
