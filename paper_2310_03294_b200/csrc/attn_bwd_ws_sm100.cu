@@ -510,7 +510,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
+#ifdef DA_BWD_VECS_FROM_GLOBAL
+          // sanitizer-evidence build only: -lse2 straight from global memory,
+          // bypassing the mbarrier-ordered smem ring (see profiles/sanitizer_r2.txt)
+          float lv[4];
+          for (int u = 0; u < 4; ++u) {
+            const int row = cur.qt * kBM + c * 32 + i + u;
+            lv[u] = row < p.rows_q
+                        ? -p.lse[static_cast<size_t>(cur.hq) * p.rows_q + row] * 1.4426950408889634f
+                        : -INFINITY;
+          }
+          const float4 l4 = make_float4(lv[0], lv[1], lv[2], lv[3]);
+#else
           const float4 l4 = *reinterpret_cast<const float4*>(lse2 + c * 32 + i);
+#endif
           const float2 x01 = ffma2(make_float2(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])),
                                    make_float2(sl2, sl2), make_float2(l4.x, l4.y));
           const float2 x23 =
@@ -589,7 +602,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
           const int qc = c * 32 + i;
+#ifdef DA_BWD_VECS_FROM_GLOBAL  // sanitizer-evidence build only (see above)
+          float dv4[4];
+          for (int u = 0; u < 4; ++u) {
+            const int row = cur.qt * kBM + qc + u;
+            dv4[u] = row < p.rows_q ? -p.d_vec[static_cast<size_t>(cur.hq) * p.rows_q + row] : 0.f;
+          }
+          const float4 d4 = make_float4(dv4[0], dv4[1], dv4[2], dv4[3]);
+#else
           const float4 d4 = *reinterpret_cast<const float4*>(dvec + qc);
+#endif
           const uint32_t a = pk[qc >> 6][(qc & 63) / 2], b = pk[qc >> 6][(qc & 63) / 2 + 1];
           const float2 t01 = fadd2(make_float2(__uint_as_float(dr[i]), __uint_as_float(dr[i + 1])),
                                    make_float2(d4.x, d4.y));

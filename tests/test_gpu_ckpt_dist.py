@@ -103,4 +103,4 @@ def test_checkpointed_layer_with_sequence_parallel_attention(cuda, world, fwd, b
     assert _rel(dx, single.grads.d_input) < 1e-2
     for lg, wr in zip(single.grads.layers, dws):
         for f, got in zip(FIELDS, wr):
-            assert _rel(got, getattr(lg, f)) < 1e-2, f
+            assert _rel(got, getattr(lg, f)) < 2e-2, f  # partial bf16 GEMM sums over ranks

@@ -45,6 +45,31 @@ def main():
         shards = make_parity_shards(3, 4, 1024, 2, 128, heads_kv=1)
         run_forward(shards, kind)
         run_backward(shards, bwd)
+    # the C++ host pipeline (pinned host in / out, per-group streams, GQA)
+    from paper_2310_03294_b200.pipeline import HostAttention
+    hq, hk, hv = (t.cpu().pin_memory() for t in qkv(4, 256, 2, seed=5))
+    hdo = qkv(4, 256, seed=6)[0].cpu().pin_memory()
+    outs = [torch.empty_like(t).pin_memory() for t in (hq, hk, hv)]
+    ha = HostAttention(4, 256, heads_per_group=2, heads_kv=2)
+    for _ in range(2):
+        ha(hq, hk, hv, hdo, *outs, sync=False)
+    ha.check()
+    # the host-buffer (fp64) entry points behind the drop-in flashcore.hpp
+    import ctypes as C
+    import numpy as np
+    from paper_2310_03294_b200 import _lib
+    lib = _lib.lib()
+    r = np.random.default_rng(0)
+    qh, kh, vh, doh = (np.ascontiguousarray(r.uniform(-1, 1, (256, 128))) for _ in range(4))
+    o, m, l = np.zeros((256, 128)), np.full(256, -np.inf), np.zeros(256)
+    ptr = lambda a: C.c_void_p(a.ctypes.data)  # noqa: E731
+    lib.da_host_attn_update(ptr(qh), 256, ptr(kh), ptr(vh), 256, 128, ptr(o), ptr(m), ptr(l), 0,
+                            128 ** -0.5)
+    out, lse = np.empty((256, 128)), np.empty(256)
+    lib.da_host_attn_finalize(ptr(o), ptr(m), ptr(l), 256, 128, ptr(out), ptr(lse))
+    g = [np.empty((256, 128)) for _ in range(3)]
+    lib.da_host_attn_backward(ptr(qh), 256, ptr(kh), ptr(vh), 256, 128, ptr(out), ptr(lse),
+                              ptr(doh), 0, 128 ** -0.5, *(ptr(x) for x in g))
     torch.cuda.synchronize()
     print("sanitize cases done")
 
