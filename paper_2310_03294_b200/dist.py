@@ -1,4 +1,12 @@
-"""One process per GPU: sequence-parallel causal attention over NCCL.
+"""Python model of the per-rank protocol (one process per rank), for the
+host-logic tests and the wall-clock trace export.
+
+The production multi-GPU path is the native per-rank runtime
+(csrc/rank_runtime.cu, ``rank.RankRuntime``), which bench.py runs. This module
+restates the same schedule-driven protocol in Python over a pluggable compute
+backend so that the CPU suite can run it under gloo, bit-exactly against the
+oracle stepper (tests/test_dist_gloo.py), and it records the reference's
+trace schema (``Recorder``/``gather_trace``, runtime.cpp:752-797).
 
 The per-rank plan comes from the native schedule (csrc/schedule.cpp, bit-exact
 with schedule.cpp:60-108); the operation order per worker is the reference's
@@ -768,180 +776,3 @@ class DistRuntime:
     def backward_trace(self, group=None):
         return gather_trace(self.rec_bwd, self.rank, self.world,
                             self.trace.get("max_remote_chunks_held_bwd", 0), group)
-
-
-# ----------------------------------------------------------------------------- bench (N > 1)
-def bench_main(args) -> int:
-    """torchrun entry for bench.py --gpus N: sequence-parallel fwd+bwd of the
-    Llama-7B attention layer at seq 32K x N (32K tokens per GPU, weak scaling);
-    messages by copy-engine pulls over NVLink (PeerTransport, default) or NCCL. Device-timed steps (barrier + synchronize on both sides, max over
-    ranks), then an e2e pass that copies each rank's q/k/v/dO shard in from
-    pinned host memory and its bf16 dq/dk/dv out inside the timed region."""
-    import json
-    import sys as _sys
-    from pathlib import Path
-
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    tdist.init_process_group("nccl", device_id=dev)
-    heads, d = args.heads, 128
-    rows = args.seq
-    n_total = rows * world
-    torch.manual_seed(1234 + rank)
-    q, k, v, do = [(torch.rand(heads, rows, d, device=dev) * 2 - 1).to(torch.bfloat16) for _ in range(4)]
-    fwd_s = getattr(args, "fwd_schedule", "balanced")
-    bwd_s = getattr(args, "bwd_schedule", "balanced")
-    native = getattr(args, "runtime", "native") == "native"
-    # the per-pass publication of pullable buffers is a host allgather: over a
-    # gloo group it is a CPU exchange; over the NCCL group it would stage
-    # through device memory and synchronise the host with the compute stream
-    boot = tdist.new_group(backend="gloo") if world > 1 else None
-    if native:
-        # the C++ per-rank runtime (csrc/rank_runtime.cu): copy-engine pulls
-        from .rank import RankRuntime
-        rt = RankRuntime(rank, world, group=boot)
-
-        def step():
-            rt.forward(q, k, v, fwd_s)
-            return rt.backward(do, bwd_s)[:3]
-    else:
-        transport = (PeerTransport(group=boot, device=dev)
-                     if getattr(args, "transport", "peer") == "peer" else None)
-        rt = DistRuntime(rank, world, device=dev, transport=transport)
-
-        def step():
-            rt.forward(q, k, v, fwd_s)
-            return rt.backward(do, bwd_s)
-
-    root = Path(__file__).resolve().parents[1]
-    if str(root) not in _sys.path:
-        _sys.path.insert(0, str(root))
-    from bench import ClockSampler, peaks  # noqa: E402  (same sampler as the N=1 arm)
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:  # started before the warm-up
-        for _ in range(args.warmup):
-            step()
-        torch.cuda.synchronize()
-        tdist.barrier()
-        clk.timed(True)
-        s.record()
-        for _ in range(args.steps):
-            step()
-        e.record()
-        torch.cuda.synchronize()
-        clk.timed(False)
-    tdist.barrier()
-    ms = torch.tensor([s.elapsed_time(e) / args.steps], device=dev)
-    tdist.all_reduce(ms, op=tdist.ReduceOp.MAX)
-    ms = ms.item()
-
-    # e2e through the same public API with host buffers. Consecutive steps
-    # overlap like a training loop with prefetch (depth 1, the reference
-    # runtime's idea applied to PCIe): step j+1's shard is copied in on one
-    # copy stream while step j computes, step j's bf16 gradients are copied
-    # out on another while step j+1 computes. Every step's copies are inside
-    # the timed region.
-    host_in = [t.cpu().pin_memory() for t in (q, k, v, do)]
-    host_out = [torch.empty(heads, rows, d, dtype=torch.bfloat16).pin_memory() for _ in range(3)]
-    dev_in = [[torch.empty_like(t) for t in (q, k, v, do)] for _ in range(2)]
-    cur = torch.cuda.current_stream()
-    h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-    freed = [None, None]  # per input set: the compute that last read it
-
-    def load(j):
-        slot = j % 2
-        with torch.cuda.stream(h2d):
-            if freed[slot] is not None:
-                h2d.wait_event(freed[slot])
-            for dst, src in zip(dev_in[slot], host_in):
-                dst.copy_(src, non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(h2d)
-        return ev
-
-    def e2e_run(n_steps):
-        h2d.wait_stream(cur)  # after the caller's timing event
-        ready = load(0)
-        for j in range(n_steps):
-            nxt = load(j + 1) if j + 1 < n_steps else None  # prefetch
-            cur.wait_event(ready)
-            x = dev_in[j % 2]
-            rt.forward(x[0], x[1], x[2], fwd_s)
-            grads = rt.backward(x[3], bwd_s)[:3]
-            g16 = [g.to(torch.bfloat16) for g in grads]
-            done = torch.cuda.Event()
-            done.record(cur)
-            freed[j % 2] = done
-            d2h.wait_event(done)
-            with torch.cuda.stream(d2h):
-                for src, dst in zip(g16, host_out):
-                    dst.copy_(src, non_blocking=True)
-                    src.record_stream(d2h)
-            ready = nxt
-        cur.wait_stream(d2h)
-
-    e2e_run(2)
-    torch.cuda.synchronize()
-    tdist.barrier()
-    e_steps = max(2, args.steps)
-    s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s2.record()
-    e2e_run(e_steps)
-    e2.record()
-    torch.cuda.synchronize()
-    tdist.barrier()
-    ms_e2e = torch.tensor([s2.elapsed_time(e2) / e_steps], device=dev)
-    tdist.all_reduce(ms_e2e, op=tdist.ReduceOp.MAX)
-    ms_e2e = ms_e2e.item()
-    fl = 7.0 * n_total * n_total * d * heads
-    peak, peak_sus, src = peaks()
-    per_gpu = fl / (ms * 1e-3) / 1e12 / world
-    # kernel launches per rank per step: one attention launch per task, a merge
-    # per received partial, finalize, preprocess + one backward launch per task
-    sched_f = {"balanced": build_balanced_schedule, "ring": build_ring_schedule,
-               "balanced_split": build_balanced_split_schedule}[fwd_s](world)
-    launches = 0
-    for st in sched_f.steps:
-        for t in st:
-            if t.kind in (TaskKind.LocalAttn, TaskKind.RemoteAttn, TaskKind.RescaleMerge):
-                launches += 1
-    sched_b = (build_balanced_backward_schedule if bwd_s == "balanced"
-               else build_ring_backward_schedule)(world)
-    for st in sched_b.steps:
-        for t in st:
-            if t.kind in (TaskKind.LocalAttn, TaskKind.RemoteAttn):
-                launches += 1
-    launches += 2 * world  # finalize + backward preprocess per rank
-    if rank == 0:
-        line = {"metric": "attn fwd+bwd TFLOP/s", "value": fl / (ms * 1e-3) / 1e12,
-                "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-                "config": {"workload": f"llama7b-attn causal fwd+bwd, {heads} heads, d=128, seq "
-                                       f"{n_total} over {world} B200 ({fwd_s} fwd + {bwd_s} bwd, "
-                                       + ("native C++ runtime, peer pulls)" if native else
-                                          f"python runtime, {getattr(args, 'transport', 'peer')} "
-                                          "transport)"),
-                           "heads": heads, "d": d, "seq_len": n_total, "tokens_per_gpu": rows,
-                           "l2": "inputs exceed L2; no flush"},
-                "tokens_per_s": n_total / (ms * 1e-3),
-                "tflops_per_gpu": per_gpu,
-                "roofline": {"bound": "tensor", "kernel": "whole step per GPU (compute + exposed "
-                             "NVLink)", "achieved": per_gpu, "peak": peak, "unit": "TFLOP/s",
-                             "frac": per_gpu / peak, "peak_source": src, "traffic": None},
-                "e2e": {"value": fl / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s",
-                        "h2d_bytes_per_step": 4 * heads * n_total * d * 2,
-                        "d2h_bytes_per_step": 3 * heads * n_total * d * 2,
-                        "ms_per_step": ms_e2e,
-                        "path": ("rank.RankRuntime (C++ da_rank_*)" if native else "dist.DistRuntime") +
-                                " forward/backward with pinned-host shards in and bf16 grads out, "
-                                "every rank; step j+1's copy-in and step j's copy-out overlap "
-                                "compute (two input sets, two copy streams)"},
-                "gpu_launches": launches * args.steps,
-                "clocks": clk.summary()}
-        print(json.dumps(line), flush=True)
-    tdist.destroy_process_group()
-    return 0

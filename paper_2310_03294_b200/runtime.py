@@ -5,8 +5,14 @@ Two executors share the reference's per-worker operation order:
 * ``run_forward`` / ``run_backward`` — P logical workers on ONE device
   (the reference's stepper, runtime.cpp:266-330 / 605-651), implemented
   natively (csrc/runtime.cu) with every chunk a sm_100a kernel.
-* ``dist.DistRuntime`` — one process per GPU over NCCL, the production path
-  (see paper_2310_03294_b200/dist.py).
+* ``rank.RankRuntime`` — one process per GPU, the production multi-GPU path:
+  the native per-rank runtime (csrc/rank_runtime.cu) with NCCL send/recv
+  (or CUDA-IPC pulls when ranks share a GPU) on a side stream.
+
+``dist.DistRuntime`` is the same protocol written in Python over a pluggable
+compute backend: it is the host-logic model the CPU suite runs under gloo
+against the oracle (tests/test_dist_gloo.py) and the wall-clock trace
+exporter; it is not what bench.py or a production caller runs.
 
 Shards are device tensors [heads, rows, 128] (bf16 q/k/v/out/d_out, fp32
 lse/dq/dk/dv).
