@@ -1,7 +1,11 @@
 // Microbenchmark: tcgen05 cta_group::2 (CTA pair, M=256) bf16 MMA throughput,
 // per SM, in clk per 128^3 GEMM-equivalent (compare tools/mb/mma_modes.cu).
 // Modes: 0 M=256 N=128 one accumulator; 1 two accumulators interleaved;
-//        2 M=256 N=256 one accumulator; 3 TS (A from TMEM) M=256 N=128 one acc.
+//        2 M=256 N=256 one accumulator; 3 TS (A from TMEM) M=256 N=128 one acc;
+//        4 TS M=256 N=128 two accumulators interleaved (the backward's dV/dK pattern);
+//        5 SS M=128 (cta_group::2: 64 rows per CTA) N=128 one accumulator;
+//        6 the backward's five-GEMM mix per iteration: SS, SS, TS, TS, SS into
+//          four accumulators (S, dP, dV, dK, dQ-like), K = 128 each.
 #include <cstdio>
 #include <cstdint>
 #include "../../paper_2310_03294_b200/csrc/sm100_ptx.cuh"
@@ -32,7 +36,7 @@ __device__ __forceinline__ void commit2(uint64_t* bar, uint16_t mask) {
                ::"r"(smem_u32(bar)), "h"(mask) : "memory");
 }
 
-constexpr int kModes = 4;
+constexpr int kModes = 7;
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) kern(long long* out, int reps) {
   extern __shared__ __align__(1024) uint8_t raw[];
   uint8_t* smem = raw + smem_align_pad(raw);
@@ -84,9 +88,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) kern(long lo
             } else if (mode == 1) {
               mma2_ss(tmem, da, db, idesc, acc);
               mma2_ss(tmem + 128, da, db, idesc, acc);
-            } else {
+            } else if (mode == 3) {
               mma2_ts(tmem, tmem + 384 + kk * 8, db, idesc, acc);
+            } else if (mode == 4) {
+              mma2_ts(tmem, tmem + 384 + kk * 8, db, idesc, acc);
+              mma2_ts(tmem + 128, tmem + 448 + kk * 8, db, idesc, acc);
+            } else if (mode == 5) {
+              mma2_ss(tmem, da, db, make_idesc_bf16(128, 128, false, false), acc);
             }
+          }
+          if (mode == 6) {  // five GEMMs, each a full K = 128 chain
+            for (int g = 0; g < 5; ++g)
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk) {
+                const uint32_t off = (kk >> 2) * kBox + (kk & 3) * 32;
+                const uint64_t da = make_sdesc_sw128(a + off, 16, 1024);
+                const uint64_t db = make_sdesc_sw128(b + off, 16, 1024);
+                const uint32_t acc = kk > 0 ? 1u : 0u;
+                const uint32_t d = tmem + (g == 4 ? 0u : static_cast<uint32_t>(g % 2) * 128u);
+                if (g == 2 || g == 3)
+                  mma2_ts(tmem + 256 + (g - 2) * 64, tmem + 384 + (g - 2) * 64 + kk * 8, db, idesc,
+                          acc);
+                else
+                  mma2_ss(d, da, db, idesc, acc);
+              }
           }
         }
         commit2(&bar, 1);
@@ -94,7 +119,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) kern(long lo
         ++phase;
         const long long dt = clock64() - t0;
         // per SM: M=256 N=128 is one 128^3 per SM per 8 steps
-        const double gemms = (mode == 1 || mode == 2) ? 2.0 * reps : 1.0 * reps;
+        const double gemms = (mode == 1 || mode == 2 || mode == 4) ? 2.0 * reps
+                             : mode == 5                           ? 0.5 * reps
+                             : mode == 6                           ? 5.0 * reps
+                                                                   : 1.0 * reps;
         const long long per = static_cast<long long>(dt / gemms);
         if (round == 0 || per < out[mode]) out[mode] = per;
       }
@@ -109,7 +137,8 @@ int main() {
   long long* d; cudaMalloc(&d, 256);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
   const char* names[kModes] = {"2CTA M256 N128 1 acc", "2CTA M256 N128 2 intl", "2CTA M256 N256 1 acc",
-                               "2CTA TS M256 N128"};
+                               "2CTA TS M256 N128", "2CTA TS M256 N128 2 intl",
+                               "2CTA M128 N128 1 acc", "2CTA bwd 5-GEMM mix"};
   for (int grid : {2, 148}) {
     kern<<<grid, 128, 200000>>>(d, 4000);
     cudaError_t e = cudaDeviceSynchronize();

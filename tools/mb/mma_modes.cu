@@ -16,7 +16,7 @@
 #include "../../paper_2310_03294_b200/csrc/sm100_ptx.cuh"
 using namespace da;
 
-constexpr int kModes = 10;
+constexpr int kModes = 11;
 __global__ void __launch_bounds__(128, 1) kern(long long* out, int reps) {
   extern __shared__ __align__(1024) uint8_t raw[];
   uint8_t* smem = raw + smem_align_pad(raw);
@@ -87,10 +87,26 @@ __global__ void __launch_bounds__(128, 1) kern(long long* out, int reps) {
               }
             } else if (mode == 2) {
               mma_ts(tmem, tmem + 384 + kk * 8, db, idesc, acc);
-            } else {
+            } else if (mode == 3) {
               mma_ts(tmem, tmem + 384 + kk * 8, db, idesc, acc);
               mma_ts(tmem + 128, tmem + 384 + kk * 8, db, idesc, acc);
             }
+          }
+          if (mode == 10) {  // the backward's five-GEMM mix: SS, SS, TS, TS, SS chains
+            for (int g = 0; g < 5; ++g)
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk) {
+                const uint32_t off = (kk >> 2) * kBox + (kk & 3) * 32;
+                const uint64_t da = make_sdesc_sw128(a + off, 16, 1024);
+                const uint64_t db = make_sdesc_sw128(b + off, 16, 1024);
+                const uint32_t acc = kk > 0 ? 1u : 0u;
+                if (g == 2 || g == 3)
+                  mma_ts(tmem + 256 + (g - 2) * 64, tmem + 384 + (g - 2) * 64 + kk * 8, db, idesc,
+                         acc);
+                else
+                  mma_ss(tmem + (g == 4 ? 0u : static_cast<uint32_t>(g % 2) * 128u), da, db, idesc,
+                         acc);
+              }
           }
           if (mode == 7 || mode == 9) {
 #pragma unroll
@@ -110,7 +126,7 @@ __global__ void __launch_bounds__(128, 1) kern(long long* out, int reps) {
         mbar_wait(&bar, phase & 1);
         ++phase;
         const long long dt = clock64() - t0;
-        const double gemms = mode == 5 ? 4.0 * reps
+        const double gemms = mode == 10 ? 5.0 * reps : mode == 5 ? 4.0 * reps
                              : (mode == 1 || mode == 3 || mode == 4 || mode >= 7) ? 2.0 * reps : 1.0 * reps;
         const long long per = static_cast<long long>(dt / gemms);
         if (round == 0 || per < out[mode]) out[mode] = per;
@@ -125,7 +141,8 @@ int main() {
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
   const char* names[kModes] = {"SS 1 accumulator", "SS 2 interleaved", "TS 1 accumulator",
                                "TS 2 interleaved", "SS N=256", "SS 4 interleaved", "SS N=64 x2",
-                               "SS 2 sequential", "SS 2 by pairs", "TS then SS"};
+                               "SS 2 sequential", "SS 2 by pairs", "TS then SS",
+                               "bwd 5-GEMM mix"};
   for (int grid : {1, 148}) {
     kern<<<grid, 128, 200000>>>(d, 4000);
     cudaError_t e = cudaDeviceSynchronize();
