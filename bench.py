@@ -264,6 +264,33 @@ def _profile_traffic():
         return {}
 
 
+# Shared-memory bytes each kernel moves per (query tile, kv tile) pair of 128 x 128
+# (DESIGN.md §4): the bound both kernels actually run against.
+#   forward  (per tile pair; a CTA owns two query tiles): S = Q K^T operands 64 KB,
+#            PV operands (P from smem) 64 KB, K/V TMA writes 32 KB, P stores 32 KB
+#   backward: MMA operands 256 KB (S 64, dP 64, dV 32, dK 32, dQ^T 64), Q/dO TMA
+#            writes 64 KB, dS stores 32 KB, dQ partial staging 128 KB (stores +
+#            TMA reads), -lse / -D broadcast loads 32 KB (8 warps x 32 x 128 B)
+SMEM_BYTES_PER_PAIR = {"fwd": 196608, "bwd": 524288}
+SMEM_B_PER_CLK_PER_SM = 128.0  # B300_MICROARCH.md "smem crossbar BW" (same SM design on B200)
+N_SM = 148
+
+
+def smem_roofline(n: int, heads: int, t_fwd_ms: float, t_bwd_ms: float, mhz) -> dict:
+    """Achieved shared-memory bandwidth per SM of both chunk kernels (causal
+    32K: n_t (n_t + 1) / 2 tile pairs per head) against 128 B/clk/SM."""
+    nt = (n + 127) // 128
+    pairs = heads * nt * (nt + 1) // 2
+    out = {"peak_B_per_clk_per_SM": SMEM_B_PER_CLK_PER_SM, "tile_pairs_per_launch": pairs,
+           "bytes_per_tile_pair": SMEM_BYTES_PER_PAIR, "clock_mhz": mhz}
+    if not mhz:
+        return out
+    for k, t in (("fwd", t_fwd_ms), ("bwd", t_bwd_ms)):
+        b = pairs * SMEM_BYTES_PER_PAIR[k] / (t * 1e-3 * mhz * 1e6 * N_SM)
+        out[k] = {"achieved_B_per_clk_per_SM": b, "frac": b / SMEM_B_PER_CLK_PER_SM}
+    return out
+
+
 def run_single(args):
     import torch
     from paper_2310_03294_b200 import flashcore as F
@@ -361,6 +388,8 @@ def run_single(args):
     dom_flops = (5.0 if dom == "bwd" else 2.0) * n * n * D * heads
     achieved = dom_flops / (t_dom * 1e-3) / 1e12
     traffic = _profile_traffic().get(f"{dom}_dram_bytes_per_launch")
+    clocks = clk.summary()
+    smem = smem_roofline(n, heads, t_fwd, t_bwd, clocks.get("sm_mhz"))
     line = {
         "metric": "attn fwd+bwd TFLOP/s", "value": tflops, "unit": "TFLOP/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -381,7 +410,8 @@ def run_single(args):
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "frac_of_sustained": achieved / peak_sus, "peak_source": src,
                      "traffic": traffic if cfg["name"] == "cfg2" else None,
-                     "algorithmic_flops_per_launch": dom_flops},
+                     "algorithmic_flops_per_launch": dom_flops,
+                     "smem": smem},
         "e2e": {"value": fl / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
                 "path": "pipeline.HostAttention -> C++ host pipeline (da_pipeline_step: fwd with "
@@ -390,7 +420,7 @@ def run_single(args):
                         "%d heads, 3 compute streams; consecutive steps overlap (step i+1's H2D of a "
                         "group waits only for step i's compute of it)" % hpg},
         "gpu_launches": 3 * args.steps,
-        "clocks": clk.summary(),
+        "clocks": clocks,
     }
     if not args.no_cpu_baseline:
         try:
