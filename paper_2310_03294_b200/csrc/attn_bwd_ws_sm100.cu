@@ -72,10 +72,17 @@ __device__ __forceinline__ unsigned long long bws_smid() {
   } while (0)
 #endif
 
+// Grid order: the CTAs of `head_group` kv heads are interleaved, so the
+// co-resident CTAs share those heads' Q / dO tiles and dQ reduction targets
+// in L2. Chosen per launch by the host (launch_attn_bwd): 2 while two heads'
+// working set (dQ fp32 + Q + dO, ~1 KB per query row) fits the 126 MB L2,
+// else 1 — e.g. the 64K x 64K Full chunk pair of cfg4 runs 1032 vs 907
+// TFLOP/s with 1 (profiles/ab_r2_bwd_head_group.txt). DA_BWD_HEAD_GROUP
+// forces a value (experiments).
 #ifndef DA_BWD_HEAD_GROUP
-#define DA_BWD_HEAD_GROUP 2
+#define DA_BWD_HEAD_GROUP 0
 #endif
-constexpr int kHeadGroup = DA_BWD_HEAD_GROUP;
+constexpr int kHeadGroupForced = DA_BWD_HEAD_GROUP;
 constexpr int kBM = 128;  // query rows per iteration
 constexpr int kBN = 128;  // kv rows per CTA
 constexpr int kHD = 128;
@@ -171,11 +178,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   // ---- work: head-major, within a head the kv tiles with most query tiles first
   const int n_q_tiles = (p.rows_q + kBM - 1) / kBM;
   const int n_kv_tiles = (p.rows_kv + kBN - 1) / kBN;
-  // kv heads in groups of kHeadGroup, interleaved within a group (L2 holds the
+  // kv heads in groups of head_group, interleaved within a group (L2 holds the
   // group's Q/dO; the last wave mixes heads instead of one head's tiles)
   const int b = static_cast<int>(blockIdx.x);
-  const int g0 = (b / (kHeadGroup * n_kv_tiles)) * kHeadGroup;
-  const int g_heads = min(kHeadGroup, p.h_kv - g0);
+  const int head_group = p.head_group;
+  const int g0 = (b / (head_group * n_kv_tiles)) * head_group;
+  const int g_heads = min(head_group, p.h_kv - g0);
   const int r_in = b - g0 * n_kv_tiles;
   const int kv_head = g0 + r_in % g_heads;
   const int slot = r_in / g_heads;
@@ -692,8 +700,15 @@ cudaError_t launch_attn_bwd(const CUtensorMap& tq, const CUtensorMap& tk, const 
   if (e != cudaSuccess) return e;
   const int n_kv_tiles = (p.rows_kv + bwdws::kBN - 1) / bwdws::kBN;
   dim3 grid(n_kv_tiles * p.h_kv);
+  BwdParams pp = p;
+  if (bwdws::kHeadGroupForced > 0) {
+    pp.head_group = bwdws::kHeadGroupForced;
+  } else {
+    constexpr double kL2Budget = 80.0 * (1 << 20);  // of the 126 MB L2
+    pp.head_group = 2.0 * static_cast<double>(p.rows_q) * 1024.0 <= kL2Budget ? 2 : 1;
+  }
   bwdws::attn_bwd_ws_kernel<<<grid, bwdws::kThreads, bwdws::kSmemBytes, stream>>>(tq, tk, tv, tdo,
-                                                                                  tdq, p);
+                                                                                  tdq, pp);
   return cudaGetLastError();
 }
 

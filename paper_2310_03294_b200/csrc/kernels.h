@@ -55,6 +55,7 @@ struct BwdParams {
   float* dk_acc;
   float* dv_acc;
   int* dq_sem;  // deterministic mode: [h_q, q tiles] zeroed counters, else nullptr
+  int head_group;  // kv heads whose CTAs are interleaved in the grid (bwd_head_group())
   unsigned long long* trace;  // DA_TRACE builds: per-iteration clock64 stamps of CTA 0
 };
 

@@ -1,6 +1,6 @@
 """Per-CTA timeline of one backward (or forward: 3rd arg "fwd") launch (DA_TRACE
 build): SM occupancy, clocks per iteration including CTA prologue/epilogue, tail.
-DISTATTN_B200_LIB=paper_2310_03294_b200/variants/lib_trace.so python tools/trace_bwd_ctas.py [n] [h] [fwd]"""
+DISTATTN_B200_LIB=paper_2310_03294_b200/variants/lib_trace.so python tools/trace_ctas.py [n] [h] [fwd|bwd] [h_kv]"""
 import ctypes as C
 import sys
 from collections import defaultdict
@@ -15,13 +15,15 @@ from paper_2310_03294_b200.flashcore import (ChunkGrads, MaskMode, backward_aux,
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 h = int(sys.argv[2]) if len(sys.argv) > 2 else 32
-q, k, v, do = [(torch.rand(h, n, 128, device="cuda") * 2 - 1).to(torch.bfloat16) for _ in range(4)]
+hkv = int(sys.argv[4]) if len(sys.argv) > 4 else h
+q, do = [(torch.rand(h, n, 128, device="cuda") * 2 - 1).to(torch.bfloat16) for _ in range(2)]
+k, v = [(torch.rand(hkv, n, 128, device="cuda") * 2 - 1).to(torch.bfloat16) for _ in range(2)]
 out = block_attn_update_final(q, k, v, None, MaskMode.Diagonal)
 dvec = backward_aux(do, out.o)
-g = ChunkGrads(torch.zeros(h, n, 128, device="cuda"), torch.empty(h, n, 128, device="cuda"),
-               torch.empty(h, n, 128, device="cuda"))
+g = ChunkGrads(torch.zeros(h, n, 128, device="cuda"), torch.empty(hkv, n, 128, device="cuda"),
+               torch.empty(hkv, n, 128, device="cuda"))
 fwd = len(sys.argv) > 3 and sys.argv[3] == "fwd"
-n_cta = h * ((n + 127) // 128) // (2 if fwd else 1)
+n_cta = h * ((n + 127) // 128) // 2 if fwd else hkv * ((n + 127) // 128)
 tr = torch.zeros(1024 + 8 * n_cta, dtype=torch.int64, device="cuda")
 if fwd:
     _lib.lib().da_debug_set_fwd_trace(C.c_void_p(tr.data_ptr()))
