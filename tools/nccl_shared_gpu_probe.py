@@ -1,3 +1,11 @@
+"""Probe: the native runtime's NCCL transport with 2+ ranks on ONE GPU.
+
+NCCL refuses it ("Duplicate GPU detected", ncclInvalidUsage at
+ncclCommInitRankConfig; gpurun_out/nccl_try.txt of the r2 probe), which is
+why the multi-rank GPU tests use the IPC transport and the NCCL protocol is
+verified on CPU (tests/test_rank_protocol.py). Kept to re-check on a box with
+several GPUs:  python tools/nccl_shared_gpu_probe.py [world]
+"""
 import os, sys, tempfile
 sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
 import numpy as np, torch, torch.multiprocessing as mp
