@@ -46,3 +46,16 @@ def test_bench_gqa_config_single_gpu(cuda):
     j = _line(r.stdout)
     assert j["config"]["heads_kv"] == 8 and j["config"]["heads"] == 32
     assert j["e2e"]["h2d_bytes_per_step"] == (2 * 32 + 2 * 8) * 4096 * 128 * 2
+
+
+def test_bench_eight_ranks_self_spawned(cuda):
+    """The SCALE run's largest N: eight self-spawned ranks (sharing cuda:0)
+    through every leg of the N>1 line."""
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "8", "--seq", "8192",
+                        "--heads", "2", "--share-gpu", "--steps", "2", "--warmup", "3",
+                        "--leg-steps", "2"], capture_output=True, text=True, timeout=900,
+                       cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-4000:]
+    j = _line(r.stdout)
+    assert j["n_gpus"] == 8 and j["config"]["tokens_per_gpu"] == 1024
+    assert {"balanced_split+balanced", "ring+ring", "balanced+balanced", "nocomm"} <= set(j["legs"])

@@ -67,10 +67,12 @@ def _rel(a, b):
     (2, 1024, 2, "balanced", "ring", None), (4, 2048, 1, "balanced", "balanced", None),
     (3, 768, 2, "ring", "balanced", None), (4, 1024, 2, "balanced_split", "ring", None),
     (1, 512, 2, "balanced", "ring", None), (2, 1002, 1, "balanced_split", "balanced", None),
-    (4, 1024, 4, "balanced", "balanced", 2)])
+    (4, 1024, 4, "balanced", "balanced", 2), (8, 2048, 2, "balanced_split", "balanced", None),
+    (8, 2048, 4, "balanced", "ring", 1)])
 def test_native_rank_runtime(cuda, world, n, heads, fwd, bwd, heads_kv):
-    """Worlds 1-4, ring / balanced / split forward, ring / balanced backward,
-    odd chunk rows (split halves 250 / 251), GQA (4 q / 2 kv heads)."""
+    """Worlds 1-4 and 8 (the SCALE run's P), ring / balanced / split forward,
+    ring / balanced backward, odd chunk rows (split halves 250 / 251), GQA
+    (4 q / 2 kv and 4 q / 1 kv heads)."""
     with tempfile.TemporaryDirectory() as td:
         mp.spawn(_worker, args=(world, _port(), n, heads, fwd, bwd, td, heads_kv), nprocs=world,
                  join=True)
