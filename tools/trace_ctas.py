@@ -57,6 +57,39 @@ for r in short:
 big = sorted(rec, key=lambda r: -r[5])[:3]
 for r in big:
     print(f"  largest CTA: {r[5]} it, {r[3] - r[2]} clk -> {(r[3] - r[2]) / max(r[5], 1):.0f} clk/it")
+# per-SM body rate (clk per iteration over the SM's CTAs, first-MMA to last
+# commit): is the spread between CTAs a property of the SM (die, TPC) or of
+# the CTA's position in the grid?
+rate = {}
+for sm, v_ in per_sm.items():
+    it_ = sum(x[5] for x in v_)
+    if it_:
+        # backward: first MMA -> last commit; forward: whole CTA (no MMA stamps)
+        rate[sm] = sum((x[3] - x[2]) if fwd else (x[7] - x[6]) for x in v_) / it_
+sms = sorted(rate)
+half = len(sms) // 2
+lo = [rate[s] for s in sms[:half]]
+hi = [rate[s] for s in sms[half:]]
+print(f"per-SM body clk/it: min {min(rate.values()):.0f} median {sorted(rate.values())[len(rate) // 2]:.0f} "
+      f"max {max(rate.values()):.0f}; SM ids < {sms[half]}: mean {sum(lo) / len(lo):.0f}, "
+      f">= : mean {sum(hi) / len(hi):.0f}")
+tpc = defaultdict(list)
+for s in sms:
+    tpc[s // 2].append(rate[s])
+pair_gap = sorted(abs(v_[0] - v_[1]) for v_ in tpc.values() if len(v_) == 2)
+print(f"|rate(SM 2t) - rate(SM 2t+1)| median {pair_gap[len(pair_gap) // 2]:.0f} clk/it")
+slow = sorted(rate, key=lambda s: -rate[s])[:12]
+print("slowest SMs:", [(s, round(rate[s])) for s in slow])
+mhz = {sm: sum(x[3] - x[2] for x in v_) / sum(x[1] - x[0] for x in v_) * 1e3
+       for sm, v_ in per_sm.items()}
+nsit = {sm: sum(x[1] - x[0] for x in v_) / max(1, sum(x[5] for x in v_)) for sm, v_ in per_sm.items()}
+fast = [s for s in sms if rate[s] < sorted(rate.values())[len(rate) // 4]]
+slow_ = [s for s in sms if rate[s] >= sorted(rate.values())[len(rate) // 2]]
+print(f"SM clock (clk64 / globaltimer): fast-quartile SMs {sum(mhz[s] for s in fast) / len(fast):.0f} MHz, "
+      f"upper-half SMs {sum(mhz[s] for s in slow_) / len(slow_):.0f} MHz; ns per iteration: "
+      f"{sum(nsit[s] for s in fast) / len(fast):.0f} vs {sum(nsit[s] for s in slow_) / len(slow_):.0f}")
+print("per-SM body clk/it by SM id:")
+print(" ".join(f"{s}:{round(rate[s])}" for s in sms))
 if fwd:
     sys.exit(0)
 pro = sorted(r[6] - r[2] for r in rec)
