@@ -384,6 +384,22 @@ da_status da_rank_backward(da_rank* r, int schedule_kind, const void* d_out, flo
  * attention backward uses its own saved O / LSE, never a recompute. */
 da_status da_rank_restore(da_rank* r, const void* q, const void* k, const void* v, void* out,
                           float* lse, int64_t h_q, int64_t h_kv, int64_t rows);
+/* Wall-clock trace (the reference's ExecutionTrace,
+ * runtime.hpp:66-89): with tracing on, every following pass records CUDA
+ * events around each task kernel and each message phase. da_rank_trace
+ * resolves the last pass of `pass` (0 forward, 1 backward) into records, times
+ * in ms from the pass origin (synchronises on the events once):
+ *   kind 0 task     code 1 local / 2 remote (direct) / 3 helper / 4 merge /
+ *                   5 fold (GradKV or dq partial); peer = the other worker
+ *   kind 1 send     code = buffer key, peer = destination rank, t0 = t1 = issue
+ *   kind 2 receive  code = buffer key, peer = source rank, t1 = arrival
+ * (step = schedule step, phase = 2t operands(t) / 2t+1 results(t); -1 for tasks). */
+typedef struct da_trace_rec {
+  int32_t kind, code, step, peer, phase, pad;
+  float t0_ms, t1_ms;
+} da_trace_rec;
+void da_rank_set_trace(da_rank* r, int on);
+da_status da_rank_trace(da_rank* r, int pass, da_trace_rec* out, int64_t cap, int64_t* n);
 /* The message protocol of one rank without a device: 5 int32 per entry
  * {pass (0 forward, 1 backward), phase (2t = operands(t), 2t+1 = results(t)),
  * dir (0 send, 1 receive), peer rank, buffer key}; *n = entries (written up to

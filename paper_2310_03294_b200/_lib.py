@@ -45,6 +45,11 @@ class RankOptions(C.Structure):
 TRANSPORT = {"ipc": 0, "nccl": 1, "none": 2}
 
 
+class TraceRec(C.Structure):
+    _fields_ = [("kind", i32), ("code", i32), ("step", i32), ("peer", i32), ("phase", i32),
+                ("pad", i32), ("t0_ms", f32), ("t1_ms", f32)]
+
+
 class Counters(C.Structure):
     _fields_ = [("kv_scalars", i64), ("q_scalars", i64), ("partial_scalars", i64),
                 ("grad_scalars", i64), ("kv_messages", i64), ("q_messages", i64),
@@ -63,6 +68,8 @@ SIGNATURES = {
     "da_stream_write_u32": (C.c_int, [vp, vp, C.c_uint32]),
     "da_rank_create": (C.c_int, [C.c_int, C.c_int, vp, vp, C.POINTER(vp)]),
     "da_rank_destroy": (None, [vp]),
+    "da_rank_set_trace": (None, [vp, C.c_int]),
+    "da_rank_trace": (C.c_int, [vp, C.c_int, vp, i64, C.POINTER(i64)]),
     "da_rank_restore": (C.c_int, [vp, vp, vp, vp, vp, vp, i64, i64, i64]),
     "da_rank_create_ex": (C.c_int, [C.c_int, C.c_int, vp, vp, vp, C.POINTER(vp)]),
     "da_rank_protocol": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(i32), i64,

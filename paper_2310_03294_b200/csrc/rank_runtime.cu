@@ -292,6 +292,19 @@ struct da_rank {
   std::array<const void*, da::kNumKeys> local{};
   std::array<size_t, da::kNumKeys> key_bytes{};
   std::set<void*> filled;  // NONE: receive slots already filled
+  // wall-clock trace of the last pass of each kind: CUDA
+  // events recorded around every task and message phase, resolved on demand
+  bool trace_on = false;
+  int trace_pass = 0;  // 0 forward, 1 backward (pass being recorded)
+  cudaEvent_t trace_origin[2] = {nullptr, nullptr};
+  struct PendingRec {
+    da_trace_rec rec;
+    cudaEvent_t e0, e1;  // e1 == e0 for instants
+  };
+  std::vector<PendingRec> pending[2];
+  std::vector<cudaEvent_t> trace_events[2];  // every event of the pass, owned once (records share them)
+  std::vector<da_trace_rec> resolved[2];
+  bool trace_ready[2] = {false, false};
   // forward state (the rematerialisation hook: saved O / LSE, never recomputed)
   const void *q = nullptr, *k = nullptr, *v = nullptr;
   void* out = nullptr;
@@ -321,6 +334,43 @@ da_status nk(ncclResult_t e, const char* where) {
     const da_status s_ = (x);        \
     if (s_ != DA_OK) return s_;      \
   } while (0)
+
+// ---- tracing (no-ops unless da_rank_set_trace enabled it)
+cudaEvent_t trace_event(da_rank* r, cudaStream_t st) {
+  if (!r->trace_on) return nullptr;
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+  cudaEventRecord(e, st);
+  r->trace_events[r->trace_pass].push_back(e);
+  return e;
+}
+
+void trace_free(da_rank* r, int pass) {
+  for (cudaEvent_t e : r->trace_events[pass]) cudaEventDestroy(e);
+  r->trace_events[pass].clear();
+  r->pending[pass].clear();
+  r->trace_origin[pass] = nullptr;  // owned by trace_events
+}
+
+void trace_push(da_rank* r, int kind, int code, int step, int peer, int phase, cudaEvent_t e0,
+                cudaEvent_t e1) {
+  if (!r->trace_on || e0 == nullptr) return;
+  da_trace_rec rec{};
+  rec.kind = kind;
+  rec.code = code;
+  rec.step = step;
+  rec.peer = peer;
+  rec.phase = phase;
+  r->pending[r->trace_pass].push_back({rec, e0, e1 ? e1 : e0});
+}
+
+void trace_begin(da_rank* r, int pass, cudaStream_t st) {
+  trace_free(r, pass);
+  r->resolved[pass].clear();
+  r->trace_ready[pass] = false;
+  r->trace_pass = pass;
+  if (r->trace_on) r->trace_origin[pass] = trace_event(r, st);
+}
 
 using AddrRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
 AddrRangeFn addr_range_fn() {
@@ -395,11 +445,16 @@ using SlotFn = void* (*)(da_rank*, const XRecv&);
 
 // Runs one phase: sends + receives of data produced (in stream order) on `cur`.
 da_status exchange(da_rank* r, const Phase& ph, void* (*slot)(da_rank*, const XRecv&),
-                   cudaStream_t cur, Work* w) {
+                   cudaStream_t cur, Work* w, int phase) {
   w->expect.clear();
   w->done = nullptr;
   if (ph.empty()) return DA_OK;
   const int tr = r->opts.transport;
+  cudaEvent_t t_issue = nullptr;  // trace: the phase is posted (sender side)
+  if (r->trace_on && tr != DA_TRANSPORT_NONE) {
+    t_issue = trace_event(r, cur);
+    for (const XSend& x : ph.sends) trace_push(r, 1, x.key, phase / 2, x.dst, phase, t_issue, t_issue);
+  }
   if (tr == DA_TRANSPORT_NONE) {  // fill each slot once from the local buffer of that kind
     for (const XRecv& x : ph.recvs) {
       void* dst = slot(r, x);
@@ -448,6 +503,10 @@ da_status exchange(da_rank* r, const Phase& ph, void* (*slot)(da_rank*, const XR
       DA_TRY(nk(n.recv(slot(r, x), r->key_bytes[x.key], ncclUint8, x.src, r->comm, r->side),
                 "ncclRecv"));
     DA_TRY(nk(n.group_end(), "ncclGroupEnd"));
+  }
+  if (t_issue != nullptr && !ph.recvs.empty()) {  // trace: the phase's data has landed
+    cudaEvent_t t_arrive = trace_event(r, r->side);
+    for (const XRecv& x : ph.recvs) trace_push(r, 2, x.key, phase / 2, x.src, phase, t_issue, t_arrive);
   }
   DA_TRY(ck(cudaEventCreateWithFlags(&w->done, cudaEventDisableTiming), "event"));
   return ck(cudaEventRecord(w->done, r->side), "event record");
@@ -652,6 +711,7 @@ da_status da_rank_create(int rank, int world, da_allgather_fn fn, void* ctx, da_
 void da_rank_destroy(da_rank* r) {
   if (r == nullptr) return;
   cudaDeviceSynchronize();
+  for (int pass = 0; pass < 2; ++pass) trace_free(r, pass);
   if (r->comm) nccl().destroy(r->comm);
   for (auto& kv : r->opened) cudaIpcCloseMemHandle(kv.second);
   for (int s = 0; s < static_cast<int>(r->rflags.size()); ++s)
@@ -734,16 +794,18 @@ da_status da_rank_forward(da_rank* r, int schedule_kind, const void* q, const vo
   bool part_pending = false;
   int held = 0;
   const int T = static_cast<int>(plans.size());
-  if (P > 1) DA_TRY(exchange(r, pg.operands[0], fwd_slot, st, &pending));
+  trace_begin(r, 0, st);
+  if (P > 1) DA_TRY(exchange(r, pg.operands[0], fwd_slot, st, &pending, 0));
   for (int t = 0; t < T; ++t) {
     const Plan& p = plans[t];
     Work next;
     const bool has_next = t + 1 < T;
     if (has_next && P > 1)  // prefetch: overlaps this step's compute
-      DA_TRY(exchange(r, pg.operands[t + 1], fwd_slot, st, &next));
+      DA_TRY(exchange(r, pg.operands[t + 1], fwd_slot, st, &next, 2 * (t + 1)));
     DA_TRY(wait_work(r, &pending, st));
     const int cur_held = (p.action >= 2 ? 1 : 0) + (has_next && plans[t + 1].action >= 2 ? 1 : 0);
     held = cur_held > held ? cur_held : held;
+    cudaEvent_t te0 = p.action ? trace_event(r, st) : nullptr;
     if (p.action == 1) {
       ++c.attention_kernel_calls;
       DA_TRY(fwd_chunk(q, k, v, h_q, h_kv, rows, rows, have_acc ? acc : nullptr, acc,
@@ -767,8 +829,10 @@ da_status da_rank_forward(da_rank* r, int schedule_kind, const void* q, const vo
       DA_TRY(fwd_chunk(r->q_slot[t % 2].p, low ? r->k_lo.p : k, low ? r->v_lo.p : v, h_q, h_kv,
                        rows, low ? lo : rows, nullptr, r->part.as<float>(), DA_MASK_FULL, st));
     }
+    if (p.action) trace_push(r, 0, p.action, t, p.action == 1 ? w : p.peer, -1, te0,
+                             trace_event(r, st));
     Work res;
-    if (P > 1) DA_TRY(exchange(r, pg.results[t], fwd_slot, st, &res));
+    if (P > 1) DA_TRY(exchange(r, pg.results[t], fwd_slot, st, &res, 2 * t + 1));
     if (p.action == 3 && p.merges.empty()) {
       part_work = res;  // the partial's send completes before r->part is rewritten
       part_pending = true;
@@ -779,9 +843,11 @@ da_status da_rank_forward(da_rank* r, int schedule_kind, const void* q, const vo
     for (int hw : p.merges) {  // in helper order (runtime.cpp:322-328, 468-474)
       count(c, kMsgPartial, nq * 130);
       const float* b = r->part_recv[hw].as<float>();
+      cudaEvent_t me0 = trace_event(r, st);
       DA_TRY(ck(launch_merge(acc, acc + nq * 128, acc + nq * 129, b, b + nq * 128, b + nq * 129,
                              acc, acc + nq * 128, acc + nq * 129, nq, st),
                 "da_rank_forward merge"));
+      trace_push(r, 0, 4, t, hw, -1, me0, trace_event(r, st));
     }
     pending = next;
   }
@@ -862,12 +928,15 @@ da_status da_rank_backward(da_rank* r, int schedule_kind, const void* d_out, flo
   da_counters c{};
   Work pending;
   const int T = static_cast<int>(plans.size());
-  if (P > 1) DA_TRY(exchange(r, pg.operands[0], bwd_slot, st, &pending));
+  trace_begin(r, 1, st);
+  if (P > 1) DA_TRY(exchange(r, pg.operands[0], bwd_slot, st, &pending, 0));
   for (int t = 0; t < T; ++t) {
     const Plan& p = plans[t];
     Work next;
-    if (t + 1 < T && P > 1) DA_TRY(exchange(r, pg.operands[t + 1], bwd_slot, st, &next));
+    if (t + 1 < T && P > 1)
+      DA_TRY(exchange(r, pg.operands[t + 1], bwd_slot, st, &next, 2 * (t + 1)));
     DA_TRY(wait_work(r, &pending, st));
+    cudaEvent_t te0 = p.action ? trace_event(r, st) : nullptr;
     if (p.action == 1) {
       ++c.attention_kernel_calls;
       DA_TRY(bwd_chunk(r->q, r->k, r->v, d_out, r->lse, r->d_vec.as<float>(), h_q, h_kv, rows, dq,
@@ -890,11 +959,14 @@ da_status da_rank_backward(da_rank* r, int schedule_kind, const void* d_out, flo
                        reinterpret_cast<const float*>(b + 2 * q_b + nq * 4), h_q, h_kv, rows, gq,
                        dk, dv, true, DA_MASK_FULL, det, st));
     }
+    if (p.action) trace_push(r, 0, p.action, t, p.action == 1 ? w : p.peer, -1, te0,
+                             trace_event(r, st));
     // results leave right after their kernels; waiting also retires the send
     // buffers before they are rewritten two steps later
     Work sw;
-    if (P > 1) DA_TRY(exchange(r, pg.results[t], bwd_slot, st, &sw));
+    if (P > 1) DA_TRY(exchange(r, pg.results[t], bwd_slot, st, &sw, 2 * t + 1));
     DA_TRY(wait_work(r, &sw, st));
+    cudaEvent_t fe0 = (!p.gradkv_from.empty() || !p.merges.empty()) ? trace_event(r, st) : nullptr;
     if (!p.gradkv_from.empty()) {
       count(c, kMsgGradKV, 2 * nkv * 128);
       DA_TRY(ck(launch_add(dk, r->g_recv.as<float>(), nkv * 128, st), "GradKV fold"));
@@ -905,6 +977,8 @@ da_status da_rank_backward(da_rank* r, int schedule_kind, const void* d_out, flo
       ++c.partial_messages;
       DA_TRY(ck(launch_add(dq, r->gq_recv[hw].as<float>(), nq * 128, st), "dq fold"));
     }
+    if (fe0) trace_push(r, 0, 5, t, p.gradkv_from.empty() ? p.merges.front() : p.gradkv_from.front(),
+                        -1, fe0, trace_event(r, st));
     pending = next;
   }
   if (counters) *counters = c;
@@ -931,6 +1005,33 @@ da_status da_rank_restore(da_rank* r, const void* q, const void* k, const void* 
   r->h_kv = h_kv;
   r->rows = rows;
   r->have_forward = true;
+  return DA_OK;
+}
+
+void da_rank_set_trace(da_rank* r, int on) {
+  if (r) r->trace_on = on != 0;
+}
+
+// Resolves the recorded events of the last pass of kind `pass` (synchronises
+// on them once) into records with times in ms relative to the pass origin.
+da_status da_rank_trace(da_rank* r, int pass, da_trace_rec* out, int64_t cap, int64_t* n) {
+  if (r == nullptr || n == nullptr || pass < 0 || pass > 1)
+    return set_error(DA_ERR_CONFIG, "da_rank_trace: bad arguments");
+  if (!r->trace_ready[pass]) {
+    if (r->trace_origin[pass] == nullptr)
+      return set_error(DA_ERR_STATE, "da_rank_trace: the pass ran without tracing");
+    for (cudaEvent_t e : r->trace_events[pass]) DA_TRY(ck(cudaEventSynchronize(e), "trace"));
+    for (auto& x : r->pending[pass]) {
+      da_trace_rec rec = x.rec;
+      DA_TRY(ck(cudaEventElapsedTime(&rec.t0_ms, r->trace_origin[pass], x.e0), "trace"));
+      DA_TRY(ck(cudaEventElapsedTime(&rec.t1_ms, r->trace_origin[pass], x.e1), "trace"));
+      r->resolved[pass].push_back(rec);
+    }
+    trace_free(r, pass);
+    r->trace_ready[pass] = true;
+  }
+  *n = static_cast<int64_t>(r->resolved[pass].size());
+  for (int64_t i = 0; out != nullptr && i < *n && i < cap; ++i) out[i] = r->resolved[pass][i];
   return DA_OK;
 }
 

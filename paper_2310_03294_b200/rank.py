@@ -56,7 +56,7 @@ class RankRuntime:
             return 1
 
     def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
-                schedule: str = "balanced", stream=None):
+                schedule: str = "balanced", stream=None, trace: bool = False):
         from .errors import ConfigError, ShapeError
         from .flashcore import _check_qkv
         _check_qkv(q, k, v, "run_forward")
@@ -71,6 +71,7 @@ class RankRuntime:
             raise ConfigError(f"unknown forward schedule {schedule!r}")
         h, rows, _ = q.shape
         hk = k.shape[0]
+        self._set_trace(trace)
         out = torch.empty_like(q)
         lse = torch.empty(h, rows, dtype=torch.float32, device=q.device)
         c = _lib.Counters()
@@ -81,7 +82,8 @@ class RankRuntime:
         self._saved = (q, k, v, out, lse)  # the runtime holds pointers to these
         return out, lse, _counters(c)
 
-    def backward(self, d_out: torch.Tensor, schedule: str = "ring", stream=None, saved=None):
+    def backward(self, d_out: torch.Tensor, schedule: str = "ring", stream=None, saved=None,
+                 trace: bool = False):
         """run_backward of this rank. `saved` = (q, k, v, out, lse) of an earlier
         forward re-installs that pass's state (a checkpointed multi-layer
         model: each layer's backward uses its own saved O / LSE); default: the
@@ -110,6 +112,7 @@ class RankRuntime:
             raise ShapeError("block_attn_backward: upstream grad shape mismatch")
         if schedule not in _BWD:
             raise ConfigError(f"unknown backward schedule {schedule!r}")
+        self._set_trace(trace)
         dq = torch.empty(q.shape, dtype=torch.float32, device=q.device)
         dk = torch.empty(k.shape, dtype=torch.float32, device=q.device)
         dv = torch.empty(k.shape, dtype=torch.float32, device=q.device)
@@ -120,6 +123,41 @@ class RankRuntime:
                                           st.cuda_stream))
         self._keep_dout = d_out
         return dq, dk, dv, _counters(c)
+
+    def _set_trace(self, on: bool):
+        if on:  # a common origin: every rank records its pass origin after the barrier
+            torch.cuda.synchronize()
+            if self.world > 1:
+                tdist.barrier(group=self.group)
+        _lib.lib().da_rank_set_trace(self._h, 1 if on else 0)
+
+    def trace_records(self, pass_: str = "forward") -> list[dict]:
+        """This rank's resolved trace records of the last traced pass."""
+        pi = {"forward": 0, "backward": 1}[pass_]
+        n = C.c_int64(0)
+        check(_lib.lib().da_rank_trace(self._h, pi, None, 0, C.byref(n)))
+        buf = (_lib.TraceRec * max(1, n.value))()
+        check(_lib.lib().da_rank_trace(self._h, pi, C.cast(buf, C.c_void_p), n.value, C.byref(n)))
+        return [{f: getattr(buf[i], f) for f, _ in _lib.TraceRec._fields_ if f != "pad"}
+                for i in range(n.value)]
+
+    def gather_trace(self, pass_: str = "forward", counters=None, held: int = 0):
+        """Collective: rank 0 gets the pass's trace in the reference schema
+        (trace_to_json, runtime.cpp:752-782 / runtime.hpp:66-89) and the other
+        ranks None. Times are ms from the pass origin (each rank's origin is
+        recorded right after a barrier). `counters`: this rank's CommCounters
+        of the pass (summed over ranks into the trace)."""
+        mine = {"rank": self.rank, "records": self.trace_records(pass_),
+                "counters": dict(counters.__dict__) if counters is not None else {},
+                "held": held}
+        allr = [None] * self.world
+        if self.world > 1:
+            tdist.all_gather_object(allr, mine, group=self.group)
+        else:
+            allr = [mine]
+        if self.rank != 0:
+            return None
+        return assemble_trace(allr, pass_)
 
     def close(self):
         if self._h:
@@ -141,3 +179,62 @@ def _counters(c) -> CommCounters:
     cc.attention_kernel_calls = c.attention_kernel_calls
     cc.max_remote_chunks_held = c.max_remote_chunks_held
     return cc
+
+
+# buffer keys of csrc/rank_runtime.cu -> the reference's PayloadKind names
+_FWD_KIND = {0: "kv", 1: "kv", 2: "q", 3: "partial", 4: "kv_half", 5: "kv_half"}
+_BWD_KIND = {0: "kv", 1: "kv", 2: "q", 6: "q", 7: "q", 8: "q", 9: "grad_kv", 10: "grad_kv",
+             11: "grad_kv", 12: "grad_kv", 13: "partial", 14: "partial"}
+_TASK = {1: "local_attn", 2: "remote_attn", 3: "helper_attn", 4: "rescale_merge", 5: "fold"}
+
+
+def _task_label(code: int, worker: int, peer: int) -> str:
+    """runtime.cpp:179-191 action_label (+ merge / fold events)."""
+    if code == 1:
+        return "local_attn"
+    if code == 2:
+        return f"remote_attn q={worker} kv={peer}"
+    if code == 3:
+        return f"helper_attn q={peer} kv={worker}"
+    if code == 4:
+        return f"rescale_merge helper={peer}"
+    return f"fold from={peer}"
+
+
+def assemble_trace(allr: list[dict], pass_: str) -> dict:
+    """Per-rank native records -> the reference's ExecutionTrace JSON shape:
+    workers[].events {t0, t1, task}, messages {t_issue (sender), t_arrive
+    (receiver), kind, from, to} (one per payload: a KV message is its k and v
+    tensors, the backward's Q message the q/dO/lse/D bundle), summed counters,
+    kernel calls, residency and makespan."""
+    kinds = _FWD_KIND if pass_ == "forward" else _BWD_KIND
+    workers, issue, arrive = [], {}, {}
+    calls = 0
+    for r in sorted(allr, key=lambda x: x["rank"]):
+        w = r["rank"] + 1
+        ev = []
+        for rec in r["records"]:
+            if rec["kind"] == 0:
+                ev.append({"t0": rec["t0_ms"], "t1": rec["t1_ms"],
+                           "task": _task_label(rec["code"], w, rec["peer"])})
+                calls += rec["code"] in (1, 2, 3)
+            elif rec["kind"] == 1:
+                key = (rec["phase"], w, rec["peer"] + 1, kinds.get(rec["code"], "?"))
+                issue[key] = min(issue.get(key, rec["t0_ms"]), rec["t0_ms"])
+            else:
+                key = (rec["phase"], rec["peer"] + 1, w, kinds.get(rec["code"], "?"))
+                arrive[key] = max(arrive.get(key, rec["t1_ms"]), rec["t1_ms"])
+        workers.append({"worker": w, "events": sorted(ev, key=lambda e: e["t0"])})
+    msgs = [{"t_issue": issue.get(k, t), "t_arrive": t, "kind": k[3], "from": k[1], "to": k[2]}
+            for k, t in arrive.items()]
+    msgs.sort(key=lambda m: (m["t_issue"], m["from"], m["to"]))
+    counters = {}
+    for r in allr:
+        for c, v in r["counters"].items():
+            if c not in ("attention_kernel_calls", "max_remote_chunks_held"):
+                counters[c] = counters.get(c, 0) + v
+    makespan = max((e["t1"] for w in workers for e in w["events"]), default=0.0)
+    return {"workers": workers, "messages": msgs, "counters": counters,
+            "attention_kernel_calls": calls,
+            "max_remote_chunks_held": max((r["held"] for r in allr), default=0),
+            "makespan": makespan, "time_unit": "ms", "clock": "CUDA events per rank"}

@@ -160,3 +160,72 @@ def test_native_rank_runtime_nocomm_arm_runs(cuda):
     q, k, v, do = O.make_inputs(0, 3, 768, 128, 2, bf16=True)
     o_r, _, _ = O.run_forward(q[0], k[0], v[0], 3, "balanced")
     assert _rel(res[0]["out"][0], o_r[:256]) < TOL
+
+
+def _trace_worker(rank, world, port, outdir, fwd, bwd):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        import json
+        from paper_2310_03294_b200.rank import RankRuntime
+        n, heads = 512 * world, 2
+        q, k, v, do = O.make_inputs(0, world, n, 128, heads, bf16=True)
+        rows = n // world
+        sl = slice(rank * rows, (rank + 1) * rows)
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a[:, sl])).cuda().to(torch.bfloat16)  # noqa: E731
+        rt = RankRuntime(rank, world, transport="ipc")
+        _, _, cf = rt.forward(t(q), t(k), t(v), fwd, trace=True)
+        _, _, _, cb = rt.backward(t(do), bwd, trace=True)
+        tf = rt.gather_trace("forward", cf, cf.max_remote_chunks_held)
+        tb = rt.gather_trace("backward", cb, cb.max_remote_chunks_held)
+        if rank == 0:
+            with open(os.path.join(outdir, "trace.json"), "w") as f:
+                json.dump({"fwd": tf, "bwd": tb}, f)
+        tdist.barrier()
+        rt.close()
+        tdist.barrier()
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,fwd,bwd", [(4, "balanced", "ring"), (4, "balanced_split", "balanced")])
+def test_native_runtime_wall_clock_trace(cuda, world, fwd, bwd):
+    """SURVEY §8(f)4 on the product path: the native runtime's CUDA-event trace
+    in the reference's ExecutionTrace schema (runtime.cpp:752-782): one event
+    per attention task and merge, one message per schedule message with the
+    schedule's (kind, from, to), arrivals after issues, counters summed."""
+    import json
+
+    from paper_2310_03294_b200 import schedule as S
+    with tempfile.TemporaryDirectory() as td:
+        mp.spawn(_trace_worker, args=(world, _port(), td, fwd, bwd), nprocs=world, join=True)
+        tr = json.load(open(os.path.join(td, "trace.json")))
+    builders = {"balanced": S.build_balanced_schedule, "ring": S.build_ring_schedule,
+                "balanced_split": S.build_balanced_split_schedule}
+    kinds = {0: "kv", 1: "q", 2: "partial", 3: "grad_kv", 4: "kv_half"}
+    sched = builders[fwd](world)
+    tf, tb = tr["fwd"], tr["bwd"]
+    for t_ in (tf, tb):
+        assert set(t_) >= {"workers", "messages", "counters", "attention_kernel_calls",
+                           "max_remote_chunks_held", "makespan"}
+        assert [w["worker"] for w in t_["workers"]] == list(range(1, world + 1))
+        for w in t_["workers"]:
+            for e in w["events"]:
+                assert 0.0 <= e["t0"] <= e["t1"] <= t_["makespan"] + 1e-3
+        for m in t_["messages"]:
+            # issue and arrival come from different ranks' clocks (origins recorded
+            # after one barrier); the ranks here share ONE GPU, whose contexts
+            # time-slice, so the origins can be milliseconds apart
+            assert m["t_issue"] >= 0.0 and 0.0 <= m["t_arrive"] <= t_["makespan"] + 50.0
+    assert sorted((m["kind"], m["from"], m["to"]) for m in tf["messages"]) == \
+        sorted((kinds[int(m.kind)], m.from_, m.to) for m in sched.messages)
+    assert tf["attention_kernel_calls"] == sched.attention_task_count()
+    merges = sum(1 for st in sched.steps for x in st if x.kind == S.TaskKind.RescaleMerge)
+    assert sum(1 for w in tf["workers"] for e in w["events"]
+               if e["task"].startswith("rescale_merge")) == merges
+    bsched = (S.build_ring_backward_schedule if bwd == "ring" else
+              S.build_balanced_backward_schedule)(world)
+    assert sorted((m["kind"], m["from"], m["to"]) for m in tb["messages"]) == \
+        sorted((kinds[int(m.kind)], m.from_, m.to) for m in bsched.messages)
+    assert tf["counters"]["kv_messages"] == sum(1 for m in sched.messages if int(m.kind) in (0, 4))
