@@ -525,6 +525,30 @@ def run_multi(args):
                                        nccl_max_ctas=args.nccl_max_ctas)
         return runtimes[tr]
 
+    fallback = None
+    if transport == "nccl":
+        # NCCL must load on every rank before any rank enters the collective
+        # communicator init; if it cannot, every rank uses the IPC pulls instead
+        from paper_2310_03294_b200.errors import Error as DaError
+        ok = torch.tensor([1.0])
+        try:
+            import ctypes as _C
+            _C.CDLL("libnccl.so.2", mode=_C.RTLD_GLOBAL)
+        except OSError as exc:
+            ok[0], fallback = 0.0, f"libnccl.so.2 not loadable: {exc}"
+        tdist.all_reduce(ok, op=tdist.ReduceOp.MIN)
+        if ok.item() > 0:
+            try:
+                runtime("nccl")
+            except DaError as exc:  # the communicator init itself failed (collective)
+                ok[0], fallback = 0.0, f"NCCL init failed: {exc}"
+            tdist.all_reduce(ok, op=tdist.ReduceOp.MIN)
+        if ok.item() == 0:
+            for rt_ in runtimes.values():
+                rt_.close()
+            runtimes.clear()
+            transport, fallback = "ipc", fallback or "NCCL failed on another rank"
+
     def timed(fwd, bwd, tr, steps, clk=None):
         rt = runtime(tr)
         res = {}
@@ -655,6 +679,7 @@ def run_multi(args):
                        "seq_len": seq, "tokens_per_gpu": rows, "fwd_schedule": head_fwd,
                        "bwd_schedule": head_bwd, "transport": transport,
                        "shared_gpu": bool(args.share_gpu),
+                       "transport_fallback": fallback,
                        "l2": "inputs exceed L2; no flush"},
             "tokens_per_s": seq / (ms * 1e-3),
             "tflops_per_gpu": per_gpu,
