@@ -21,7 +21,9 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <initializer_list>
 #include <limits>
+#include <string>
 
 #include "capi_internal.h"
 #include "kernels.h"
@@ -127,6 +129,12 @@ da_status download(HostCtx* c, size_t off, size_t bytes) {
     if (s_ != DA_OK) return s_;   \
   } while (0)
 
+bool any_null(std::initializer_list<const void*> ps) {
+  for (const void* p : ps)
+    if (p == nullptr) return true;
+  return false;
+}
+
 da_status check_dims(int64_t rows_q, int64_t rows_kv, int64_t d, const char* op) {
   if (d != 128) return set_error(DA_ERR_UNSUPPORTED, std::string(op) + ": d must be 128");
   if (rows_q < 0 || rows_kv < 0) return set_error(DA_ERR_SHAPE, std::string(op) + ": bad rows");
@@ -149,6 +157,8 @@ extern "C" {
 da_status da_host_attn_update(const double* q, int64_t rows_q, const double* k, const double* v,
                               int64_t rows_kv, int64_t d, double* o, double* m, double* l,
                               int mask, double scale) {
+  if (any_null({q, k, v, o, m, l}))
+    return set_error(DA_ERR_CONFIG, "block_attn_update: null host buffer");
   HOST_TRY(check_dims(rows_q, rows_kv, d, "block_attn_update"));
   if (mask == DA_MASK_EMPTY || rows_q == 0 || rows_kv == 0) return DA_OK;  // no-op (:148)
   if (mask == DA_MASK_DIAGONAL && rows_q != rows_kv)
@@ -202,6 +212,8 @@ da_status da_host_attn_merge(const double* o_a, const double* m_a, const double*
                              const double* o_b, const double* m_b, const double* l_b,
                              double* o_out, double* m_out, double* l_out, int64_t rows,
                              int64_t d) {
+  if (any_null({o_a, m_a, l_a, o_b, m_b, l_b, o_out, m_out, l_out}))
+    return set_error(DA_ERR_CONFIG, "rescale: null host buffer");
   HOST_TRY(check_dims(rows, rows, d, "rescale"));
   if (rows == 0) return DA_OK;
   const int64_t n = rows * d;
@@ -229,6 +241,8 @@ da_status da_host_attn_merge(const double* o_a, const double* m_a, const double*
 
 da_status da_host_attn_finalize(const double* o, const double* m, const double* l, int64_t rows,
                                 int64_t d, double* out, double* lse) {
+  if (any_null({o, m, l, out, lse}))
+    return set_error(DA_ERR_CONFIG, "finalize: null host buffer");
   HOST_TRY(check_dims(rows, rows, d, "finalize"));
   if (rows == 0) return DA_OK;
   const int64_t n = rows * d;
@@ -256,6 +270,8 @@ da_status da_host_attn_finalize(const double* o, const double* m, const double* 
 
 da_status da_host_backward_aux(const double* d_out, const double* out, int64_t rows, int64_t d,
                                double* d_vec) {
+  if (any_null({d_out, out, d_vec}))
+    return set_error(DA_ERR_CONFIG, "backward_aux: null host buffer");
   HOST_TRY(check_dims(rows, rows, d, "backward_aux"));
   if (rows == 0) return DA_OK;
   const int64_t n = rows * d;
@@ -277,6 +293,8 @@ da_status da_host_attn_backward(const double* q, int64_t rows_q, const double* k
                                 const double* v, int64_t rows_kv, int64_t d, const double* out,
                                 const double* lse, const double* d_out, int mask, double scale,
                                 double* dq, double* dk, double* dv) {
+  if (any_null({q, k, v, out, lse, d_out, dq, dk, dv}))
+    return set_error(DA_ERR_CONFIG, "block_attn_backward: null host buffer");
   HOST_TRY(check_dims(rows_q, rows_kv, d, "block_attn_backward"));
   const int64_t nq = rows_q * d, nk = rows_kv * d;
   if (mask == DA_MASK_EMPTY || rows_q == 0 || rows_kv == 0) {  // zero contribution (:292)
@@ -334,6 +352,8 @@ da_status da_host_attn_backward(const double* q, int64_t rows_q, const double* k
 da_status da_host_dense_attention(const double* q, int64_t rows_q, const double* k,
                                   const double* v, int64_t rows_kv, int64_t d, int causal,
                                   double scale, double* out, double* lse) {
+  if (any_null({q, k, v, out, lse}))
+    return set_error(DA_ERR_CONFIG, "dense_oracle: null host buffer");
   HOST_TRY(check_dims(rows_q, rows_kv, d, "dense_oracle"));
   if (causal && rows_q != rows_kv)
     return set_error(DA_ERR_SHAPE, "dense_oracle: causal attention needs a square chunk");

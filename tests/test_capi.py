@@ -52,3 +52,20 @@ def test_argument_errors_without_device():
     b = _lib.BwdArgs()
     b.d, b.h_q, b.h_kv, b.rows_q, b.rows_kv, b.mask = 128, 2, 2, 128, 128, 1
     assert lib.da_attn_bwd_chunk(C.byref(b), None) == 4  # StateError: no lse / D
+
+
+def test_host_entry_points_validate_before_device_work():
+    """The drop-in's host-buffer entry points (da_host_*) reject null buffers,
+    d != 128 and non-square diagonal chunks without touching a device."""
+    import ctypes as C
+
+    import numpy as np
+    lib = _lib.lib()
+    buf = np.zeros((128, 64))
+    p = C.c_void_p(buf.ctypes.data)
+    assert lib.da_host_attn_update(None, 128, p, p, 128, 128, p, p, p, 0, 0.1) == 2
+    assert b"null host buffer" in lib.da_last_error()
+    assert lib.da_host_attn_update(p, 128, p, p, 128, 64, p, p, p, 0, 0.1) == 8  # d != 128
+    assert lib.da_host_attn_update(p, 128, p, p, 64, 128, p, p, p, 0, 0.1) == 1  # diagonal
+    assert lib.da_host_attn_backward(p, 128, p, p, 128, 128, p, p, None, 1, 0.1, p, p, p) == 2
+    assert lib.da_host_attn_update(p, 128, p, p, 128, 128, p, p, p, 2, 0.1) == 0  # Empty: no-op

@@ -59,3 +59,16 @@ def test_bench_eight_ranks_self_spawned(cuda):
     j = _line(r.stdout)
     assert j["n_gpus"] == 8 and j["config"]["tokens_per_gpu"] == 1024
     assert {"balanced_split+balanced", "ring+ring", "balanced+balanced", "nocomm"} <= set(j["legs"])
+
+
+def test_bench_nccl_failure_falls_back_to_ipc(cuda):
+    """--transport nccl with both ranks on one GPU: NCCL's communicator init
+    fails on every rank (duplicate GPU); the ranks agree and run the IPC
+    transport instead, and the line records why."""
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--seq", "4096",
+                        "--heads", "2", "--share-gpu", "--transport", "nccl", "--steps", "2",
+                        "--warmup", "3", "--no-legs"], capture_output=True, text=True, timeout=600,
+                       cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-4000:]
+    j = _line(r.stdout)
+    assert j["config"]["transport"] == "ipc" and "NCCL" in j["config"]["transport_fallback"]
