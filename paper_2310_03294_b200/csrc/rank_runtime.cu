@@ -189,11 +189,13 @@ da_status backward_program(const FlatSchedule& s, int worker, Program* out) {
     const Key gq = (t % 2) ? kGQ1 : kGQ0;
     if (p.action == 2) res.sends.insert(res.sends.end(), {{p.peer - 1, gk}, {p.peer - 1, gv}});
     if (p.action == 3) res.sends.push_back({p.peer - 1, gq});
+    // receive slots alternate by step parity: results(t) are folded during
+    // step t+1 (after its kernel is queued), while results(t+1) may land
     for (int src : p.gradkv_from) {
-      res.recvs.push_back({src - 1, gk, kSlotGrad, 0, 0});
-      res.recvs.push_back({src - 1, gv, kSlotGrad, 0, 1});
+      res.recvs.push_back({src - 1, gk, kSlotGrad, t % 2, 0});
+      res.recvs.push_back({src - 1, gv, kSlotGrad, t % 2, 1});
     }
-    for (int hw : p.merges) res.recvs.push_back({hw - 1, gq, kSlotGQ, hw, 0});
+    for (int hw : p.merges) res.recvs.push_back({hw - 1, gq, kSlotGQ, 2 * hw + t % 2, 0});
   }
   *out = std::move(pg);
   return DA_OK;
@@ -314,7 +316,7 @@ struct da_rank {
   // work buffers
   da::Buf acc, part, kv_slot[2], q_slot[2], k_lo, v_lo, k_hi, v_hi, kvh, flag;
   std::map<int, da::Buf> part_recv, gq_recv;
-  da::Buf d_vec, bundle[2], g_send[2], q_send[2], g_recv;
+  da::Buf d_vec, bundle[2], g_send[2], q_send[2], g_recv[2];
 };
 
 namespace da {
@@ -629,7 +631,7 @@ void* bwd_slot(da_rank* r, const XRecv& x) {
   switch (x.slot) {
     case kSlotKV: return r->kv_slot[x.index].as<char>() + x.part * kv_b;
     case kSlotBundle: return r->bundle[x.index].as<char>() + bundle_off[x.part];
-    case kSlotGrad: return r->g_recv.as<char>() + x.part * g_kv;
+    case kSlotGrad: return r->g_recv[x.index].as<char>() + x.part * g_kv;
     case kSlotGQ: return r->gq_recv[x.index].p;
     default: return nullptr;
   }
@@ -897,9 +899,10 @@ da_status da_rank_backward(da_rank* r, int schedule_kind, const void* d_out, flo
     DA_TRY(ck(r->g_send[i].ensure(2 * g_kv), "da_rank workspace"));
     DA_TRY(ck(r->q_send[i].ensure(g_q), "da_rank workspace"));
   }
-  DA_TRY(ck(r->g_recv.ensure(2 * g_kv), "da_rank workspace"));
-  for (const Plan& p : plans)
-    for (int hw : p.merges) DA_TRY(ck(r->gq_recv[hw].ensure(g_q), "da_rank workspace"));
+  for (int i = 0; i < 2; ++i) DA_TRY(ck(r->g_recv[i].ensure(2 * g_kv), "da_rank workspace"));
+  for (size_t t = 0; t < plans.size(); ++t)
+    for (int hw : plans[t].merges)
+      DA_TRY(ck(r->gq_recv[2 * hw + static_cast<int>(t % 2)].ensure(g_q), "da_rank workspace"));
   DA_TRY(ck(cudaMemsetAsync(dq, 0, g_q, st), "dq zero"));
   DA_TRY(ck(cudaMemsetAsync(dk, 0, g_kv, st), "dk zero"));
   DA_TRY(ck(cudaMemsetAsync(dv, 0, g_kv, st), "dv zero"));
@@ -928,6 +931,31 @@ da_status da_rank_backward(da_rank* r, int schedule_kind, const void* d_out, flo
   da_counters c{};
   Work pending;
   const int T = static_cast<int>(plans.size());
+  Work res_w[2];
+  // waits for step tt's results phase and folds what it brought (GradKV into
+  // dk / dv, helpers' dq partials into dq), in schedule order
+  auto complete = [&](int tt) -> da_status {
+    const Plan& pp = plans[tt];
+    DA_TRY(wait_work(r, &res_w[tt % 2], st));
+    cudaEvent_t fe0 =
+        (!pp.gradkv_from.empty() || !pp.merges.empty()) ? trace_event(r, st) : nullptr;
+    if (!pp.gradkv_from.empty()) {
+      count(c, kMsgGradKV, 2 * nkv * 128);
+      const float* g = r->g_recv[tt % 2].as<float>();
+      DA_TRY(ck(launch_add(dk, g, nkv * 128, st), "GradKV fold"));
+      DA_TRY(ck(launch_add(dv, g + nkv * 128, nkv * 128, st), "GradKV fold"));
+    }
+    for (int hw : pp.merges) {
+      c.partial_scalars += nq * 128;
+      ++c.partial_messages;
+      DA_TRY(ck(launch_add(dq, r->gq_recv[2 * hw + tt % 2].as<float>(), nq * 128, st),
+                "dq fold"));
+    }
+    if (fe0)
+      trace_push(r, 0, 5, tt, pp.gradkv_from.empty() ? pp.merges.front() : pp.gradkv_from.front(),
+                 -1, fe0, trace_event(r, st));
+    return DA_OK;
+  };
   trace_begin(r, 1, st);
   if (P > 1) DA_TRY(exchange(r, pg.operands[0], bwd_slot, st, &pending, 0));
   for (int t = 0; t < T; ++t) {
@@ -961,26 +989,16 @@ da_status da_rank_backward(da_rank* r, int schedule_kind, const void* d_out, flo
     }
     if (p.action) trace_push(r, 0, p.action, t, p.action == 1 ? w : p.peer, -1, te0,
                              trace_event(r, st));
-    // results leave right after their kernels; waiting also retires the send
-    // buffers before they are rewritten two steps later
-    Work sw;
-    if (P > 1) DA_TRY(exchange(r, pg.results[t], bwd_slot, st, &sw, 2 * t + 1));
-    DA_TRY(wait_work(r, &sw, st));
-    cudaEvent_t fe0 = (!p.gradkv_from.empty() || !p.merges.empty()) ? trace_event(r, st) : nullptr;
-    if (!p.gradkv_from.empty()) {
-      count(c, kMsgGradKV, 2 * nkv * 128);
-      DA_TRY(ck(launch_add(dk, r->g_recv.as<float>(), nkv * 128, st), "GradKV fold"));
-      DA_TRY(ck(launch_add(dv, r->g_recv.as<float>() + nkv * 128, nkv * 128, st), "GradKV fold"));
-    }
-    for (int hw : p.merges) {
-      c.partial_scalars += nq * 128;
-      ++c.partial_messages;
-      DA_TRY(ck(launch_add(dq, r->gq_recv[hw].as<float>(), nq * 128, st), "dq fold"));
-    }
-    if (fe0) trace_push(r, 0, 5, t, p.gradkv_from.empty() ? p.merges.front() : p.gradkv_from.front(),
-                        -1, fe0, trace_event(r, st));
+    // results leave right after their kernels. They are completed one step
+    // later (after step t+1's kernel is queued): the transfer of GradKV / dq
+    // partials overlaps the next kernel instead of stalling the compute
+    // stream, and the send buffers (double-buffered) are retired before
+    // step t+2 rewrites them. Folds keep the ascending-sender order.
+    if (P > 1) DA_TRY(exchange(r, pg.results[t], bwd_slot, st, &res_w[t % 2], 2 * t + 1));
+    if (t >= 1) DA_TRY(complete(t - 1));
     pending = next;
   }
+  if (T >= 1) DA_TRY(complete(T - 1));
   if (counters) *counters = c;
   return DA_OK;
 }
