@@ -378,6 +378,18 @@ da_status da_rank_forward(da_rank* r, int schedule_kind, const void* q, const vo
                           float* lse, da_counters* counters, void* stream);
 da_status da_rank_backward(da_rank* r, int schedule_kind, const void* d_out, float* dq, float* dk,
                            float* dv, da_counters* counters, void* stream);
+/* The same passes over a caller-supplied validated schedule table (the flat
+ * encoding of da_schedule_build; runtime.hpp:106-118 take `const Schedule&`).
+ * Every rank must pass the same table. */
+da_status da_rank_forward_table(da_rank* r, int32_t steps, const int32_t* tasks, int64_t n_tasks,
+                                const int32_t* messages, int64_t n_messages, const void* q,
+                                const void* k, const void* v, int64_t h_q, int64_t h_kv,
+                                int64_t rows, void* out, float* lse, da_counters* counters,
+                                void* stream);
+da_status da_rank_backward_table(da_rank* r, int32_t steps, const int32_t* tasks, int64_t n_tasks,
+                                 const int32_t* messages, int64_t n_messages, const void* d_out,
+                                 float* dq, float* dk, float* dv, da_counters* counters,
+                                 void* stream);
 /* Re-installs a saved forward state (this rank's q, k, v, O, LSE of an
  * earlier pass) for the next da_rank_backward — the rematerialisation hook
  * of a checkpointed multi-layer model (ckptplan.cpp:198-206): each layer's

@@ -70,6 +70,10 @@ SIGNATURES = {
     "da_rank_destroy": (None, [vp]),
     "da_rank_set_trace": (None, [vp, C.c_int]),
     "da_rank_trace": (C.c_int, [vp, C.c_int, vp, i64, C.POINTER(i64)]),
+    "da_rank_forward_table": (C.c_int, [vp, i32, C.POINTER(i32), i64, C.POINTER(i32), i64, vp,
+                                        vp, vp, i64, i64, i64, vp, vp, vp, vp]),
+    "da_rank_backward_table": (C.c_int, [vp, i32, C.POINTER(i32), i64, C.POINTER(i32), i64, vp,
+                                         vp, vp, vp, vp, vp]),
     "da_rank_restore": (C.c_int, [vp, vp, vp, vp, vp, vp, i64, i64, i64]),
     "da_rank_create_ex": (C.c_int, [C.c_int, C.c_int, vp, vp, vp, C.POINTER(vp)]),
     "da_rank_protocol": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(i32), i64,

@@ -723,16 +723,15 @@ void da_rank_destroy(da_rank* r) {
   delete r;
 }
 
-da_status da_rank_forward(da_rank* r, int schedule_kind, const void* q, const void* k,
-                          const void* v, int64_t h_q, int64_t h_kv, int64_t rows, void* out,
-                          float* lse, da_counters* counters, void* stream) {
-  if (r == nullptr) return set_error(DA_ERR_CONFIG, "da_rank_forward: null runtime");
+static da_status rank_forward_flat(da_rank* r, const FlatSchedule& sch, const void* q,
+                                   const void* k, const void* v, int64_t h_q, int64_t h_kv,
+                                   int64_t rows, void* out, float* lse, da_counters* counters,
+                                   void* stream) {
   if (h_q < 1 || h_kv < 1 || h_q % h_kv != 0 || rows < 1)
     return set_error(DA_ERR_SHAPE, "da_rank_forward: bad shape");
   const int P = r->world, w = r->rank + 1;
-  bool ok = false;
-  const FlatSchedule sch = forward_table(schedule_kind, P, &ok);
-  if (!ok) return set_error(DA_ERR_CONFIG, "da_rank_forward: unknown schedule kind");
+  if (sch.workers != P)
+    return set_error(DA_ERR_SCHEDULE, "schedule worker count does not match the world size");
   const auto errs = validate_flat(sch);
   if (!errs.empty()) return set_error(DA_ERR_SCHEDULE, "invalid schedule: " + errs.front());
   Program pg;
@@ -870,16 +869,15 @@ da_status da_rank_forward(da_rank* r, int schedule_kind, const void* q, const vo
   return da_check_degenerate(r->flag.as<int>(), stream);
 }
 
-da_status da_rank_backward(da_rank* r, int schedule_kind, const void* d_out, float* dq, float* dk,
-                           float* dv, da_counters* counters, void* stream) {
-  if (r == nullptr) return set_error(DA_ERR_CONFIG, "da_rank_backward: null runtime");
+static da_status rank_backward_flat(da_rank* r, const FlatSchedule& sch, const void* d_out,
+                                    float* dq, float* dk, float* dv, da_counters* counters,
+                                    void* stream) {
   if (!r->have_forward)
     return set_error(DA_ERR_STATE, "run_backward requires forward output and logsumexp");
   if (d_out == nullptr) return set_error(DA_ERR_STATE, "run_backward requires d_out");
   const int P = r->world, w = r->rank + 1;
-  bool ok = false;
-  const FlatSchedule sch = backward_table(schedule_kind, P, &ok);
-  if (!ok) return set_error(DA_ERR_CONFIG, "da_rank_backward: unknown schedule kind");
+  if (sch.workers != P)
+    return set_error(DA_ERR_SCHEDULE, "schedule worker count does not match the world size");
   const auto errs = validate_backward_flat(sch);
   if (!errs.empty()) return set_error(DA_ERR_SCHEDULE, "invalid schedule: " + errs.front());
   Program pg;
@@ -1024,6 +1022,60 @@ da_status da_rank_restore(da_rank* r, const void* q, const void* k, const void* 
   r->rows = rows;
   r->have_forward = true;
   return DA_OK;
+}
+
+static FlatSchedule rank_table(int workers, int32_t steps, const int32_t* tasks,
+                               int64_t n_tasks, const int32_t* messages, int64_t n_messages) {
+  FlatSchedule f;
+  f.workers = workers;
+  f.steps = steps;
+  for (int64_t i = 0; tasks && i < n_tasks; ++i) {
+    const int32_t* o = tasks + 6 * i;
+    f.tasks.push_back({o[0], o[1], o[2], o[3], o[4], o[5]});
+  }
+  for (int64_t i = 0; messages && i < n_messages; ++i) {
+    const int32_t* o = messages + 4 * i;
+    f.messages.push_back({o[0], o[1], o[2], o[3]});
+  }
+  return f;
+}
+
+da_status da_rank_forward(da_rank* r, int schedule_kind, const void* q, const void* k,
+                          const void* v, int64_t h_q, int64_t h_kv, int64_t rows, void* out,
+                          float* lse, da_counters* counters, void* stream) {
+  if (r == nullptr) return set_error(DA_ERR_CONFIG, "da_rank_forward: null runtime");
+  bool ok = false;
+  const FlatSchedule sch = forward_table(schedule_kind, r->world, &ok);
+  if (!ok) return set_error(DA_ERR_CONFIG, "da_rank_forward: unknown schedule kind");
+  return rank_forward_flat(r, sch, q, k, v, h_q, h_kv, rows, out, lse, counters, stream);
+}
+
+da_status da_rank_forward_table(da_rank* r, int32_t steps, const int32_t* tasks, int64_t n_tasks,
+                                const int32_t* messages, int64_t n_messages, const void* q,
+                                const void* k, const void* v, int64_t h_q, int64_t h_kv,
+                                int64_t rows, void* out, float* lse, da_counters* counters,
+                                void* stream) {
+  if (r == nullptr) return set_error(DA_ERR_CONFIG, "da_rank_forward: null runtime");
+  return rank_forward_flat(r, rank_table(r->world, steps, tasks, n_tasks, messages, n_messages),
+                           q, k, v, h_q, h_kv, rows, out, lse, counters, stream);
+}
+
+da_status da_rank_backward(da_rank* r, int schedule_kind, const void* d_out, float* dq, float* dk,
+                           float* dv, da_counters* counters, void* stream) {
+  if (r == nullptr) return set_error(DA_ERR_CONFIG, "da_rank_backward: null runtime");
+  bool ok = false;
+  const FlatSchedule sch = backward_table(schedule_kind, r->world, &ok);
+  if (!ok) return set_error(DA_ERR_CONFIG, "da_rank_backward: unknown schedule kind");
+  return rank_backward_flat(r, sch, d_out, dq, dk, dv, counters, stream);
+}
+
+da_status da_rank_backward_table(da_rank* r, int32_t steps, const int32_t* tasks, int64_t n_tasks,
+                                 const int32_t* messages, int64_t n_messages, const void* d_out,
+                                 float* dq, float* dk, float* dv, da_counters* counters,
+                                 void* stream) {
+  if (r == nullptr) return set_error(DA_ERR_CONFIG, "da_rank_backward: null runtime");
+  return rank_backward_flat(r, rank_table(r->world, steps, tasks, n_tasks, messages, n_messages),
+                            d_out, dq, dk, dv, counters, stream);
 }
 
 void da_rank_set_trace(da_rank* r, int on) {

@@ -67,7 +67,7 @@ class RankRuntime:
             raise ShapeError("all shards must share the same q/k/v shape")
         if q.shape[0] % k.shape[0] != 0:
             raise ShapeError("h_q must be a positive multiple of h_kv")
-        if schedule not in _FWD:
+        if isinstance(schedule, str) and schedule not in _FWD:
             raise ConfigError(f"unknown forward schedule {schedule!r}")
         h, rows, _ = q.shape
         hk = k.shape[0]
@@ -76,9 +76,17 @@ class RankRuntime:
         lse = torch.empty(h, rows, dtype=torch.float32, device=q.device)
         c = _lib.Counters()
         st = stream if stream is not None else torch.cuda.current_stream()
-        check(_lib.lib().da_rank_forward(self._h, _FWD[schedule], q.data_ptr(), k.data_ptr(),
-                                         v.data_ptr(), h, hk, rows, out.data_ptr(),
-                                         lse.data_ptr(), C.byref(c), st.cuda_stream))
+        if isinstance(schedule, str):
+            check(_lib.lib().da_rank_forward(self._h, _FWD[schedule], q.data_ptr(), k.data_ptr(),
+                                             v.data_ptr(), h, hk, rows, out.data_ptr(),
+                                             lse.data_ptr(), C.byref(c), st.cuda_stream))
+        else:  # a validated Schedule object (runtime.hpp:106-109), the same on every rank
+            from .runtime import _table
+            steps, t, nt, m, nm = _table(schedule)
+            check(_lib.lib().da_rank_forward_table(self._h, steps, t, nt, m, nm, q.data_ptr(),
+                                                   k.data_ptr(), v.data_ptr(), h, hk, rows,
+                                                   out.data_ptr(), lse.data_ptr(), C.byref(c),
+                                                   st.cuda_stream))
         self._saved = (q, k, v, out, lse)  # the runtime holds pointers to these
         return out, lse, _counters(c)
 
@@ -110,7 +118,7 @@ class RankRuntime:
         _req(d_out, torch.bfloat16, "d_out")
         if d_out.shape != q.shape:
             raise ShapeError("block_attn_backward: upstream grad shape mismatch")
-        if schedule not in _BWD:
+        if isinstance(schedule, str) and schedule not in _BWD:
             raise ConfigError(f"unknown backward schedule {schedule!r}")
         self._set_trace(trace)
         dq = torch.empty(q.shape, dtype=torch.float32, device=q.device)
@@ -118,9 +126,17 @@ class RankRuntime:
         dv = torch.empty(k.shape, dtype=torch.float32, device=q.device)
         c = _lib.Counters()
         st = stream if stream is not None else torch.cuda.current_stream()
-        check(_lib.lib().da_rank_backward(self._h, _BWD[schedule], d_out.data_ptr(), dq.data_ptr(),
-                                          dk.data_ptr(), dv.data_ptr(), C.byref(c),
-                                          st.cuda_stream))
+        if isinstance(schedule, str):
+            check(_lib.lib().da_rank_backward(self._h, _BWD[schedule], d_out.data_ptr(),
+                                              dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
+                                              C.byref(c), st.cuda_stream))
+        else:
+            from .runtime import _table
+            steps, t, nt, m, nm = _table(schedule)
+            check(_lib.lib().da_rank_backward_table(self._h, steps, t, nt, m, nm,
+                                                    d_out.data_ptr(), dq.data_ptr(),
+                                                    dk.data_ptr(), dv.data_ptr(), C.byref(c),
+                                                    st.cuda_stream))
         self._keep_dout = d_out
         return dq, dk, dv, _counters(c)
 

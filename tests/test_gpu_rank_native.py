@@ -229,3 +229,50 @@ def test_native_runtime_wall_clock_trace(cuda, world, fwd, bwd):
     assert sorted((m["kind"], m["from"], m["to"]) for m in tb["messages"]) == \
         sorted((kinds[int(m.kind)], m.from_, m.to) for m in bsched.messages)
     assert tf["counters"]["kv_messages"] == sum(1 for m in sched.messages if int(m.kind) in (0, 4))
+
+
+def _table_worker(rank, world, port, outdir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import dataclasses
+        torch.cuda.set_device(0)
+        from paper_2310_03294_b200 import schedule as S
+        from paper_2310_03294_b200.rank import RankRuntime
+        n, heads = 256 * world, 2
+        q, k, v, do = O.make_inputs(0, world, n, 128, heads, bf16=True)
+        rows = n // world
+        sl = slice(rank * rows, (rank + 1) * rows)
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a[:, sl])).cuda().to(torch.bfloat16)  # noqa: E731
+        custom = S.build_ring_schedule(world)  # a valid table none of the built-ins: steps 1, 2 swapped
+        custom.steps[1], custom.steps[2] = custom.steps[2], custom.steps[1]
+        custom.messages = sorted((dataclasses.replace(m, step=3 - m.step) if m.step in (1, 2) else m
+                                  for m in custom.messages), key=lambda m: (m.step, m.from_))
+        rt = RankRuntime(rank, world, transport="ipc")
+        out, lse, _ = rt.forward(t(q), t(k), t(v), custom)
+        dq, dk, dv, _ = rt.backward(t(do), S.build_ring_backward_schedule(world))
+        torch.cuda.synchronize()
+        np.savez(os.path.join(outdir, f"r{rank}.npz"), out=out.float().cpu().numpy(),
+                 lse=lse.cpu().numpy(), dq=dq.cpu().numpy())
+        tdist.barrier()
+        rt.close()
+        tdist.barrier()
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_native_runtime_takes_schedule_tables(cuda):
+    """da_rank_forward_table / da_rank_backward_table: any validated table (here
+    ring with steps 1 and 2 swapped, and the ring backward as an object) runs
+    on the per-rank runtime and matches the oracle's ring results."""
+    world = 4
+    with tempfile.TemporaryDirectory() as td:
+        mp.spawn(_table_worker, args=(world, _port(), td), nprocs=world, join=True)
+        res = [np.load(os.path.join(td, f"r{r}.npz")) for r in range(world)]
+    got = {f: np.concatenate([r[f] for r in res], axis=1) for f in ("out", "lse", "dq")}
+    q, k, v, do = O.make_inputs(0, world, 256 * world, 128, 2, bf16=True)
+    for h in range(2):
+        o_r, l_r, _ = O.run_forward(q[h], k[h], v[h], world, "ring")
+        dq_r = O.run_backward(q[h], k[h], v[h], o_r, l_r, do[h], world)[0]
+        assert _rel(got["out"][h], o_r) < TOL and np.abs(got["lse"][h] - l_r).max() < LSE_TOL
+        assert _rel(got["dq"][h], dq_r) < TOL
