@@ -16,6 +16,7 @@ from paper_2310_03294_b200.flashcore import (ChunkGrads, MaskMode, backward_aux,
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 h = int(sys.argv[2]) if len(sys.argv) > 2 else 32
 hkv = int(sys.argv[4]) if len(sys.argv) > 4 else h
+det = len(sys.argv) > 5 and sys.argv[5] == "det"  # deterministic dQ order
 q, do = [(torch.rand(h, n, 128, device="cuda") * 2 - 1).to(torch.bfloat16) for _ in range(2)]
 k, v = [(torch.rand(hkv, n, 128, device="cuda") * 2 - 1).to(torch.bfloat16) for _ in range(2)]
 out = block_attn_update_final(q, k, v, None, MaskMode.Diagonal)
@@ -32,7 +33,8 @@ if fwd:
 else:
     _lib.lib().da_debug_set_bwd_trace(C.c_void_p(tr.data_ptr()))
     for _ in range(3):
-        block_attn_backward(q, k, v, out.o, out.lse, do, MaskMode.Diagonal, d_vec=dvec, grads=g)
+        block_attn_backward(q, k, v, out.o, out.lse, do, MaskMode.Diagonal, d_vec=dvec, grads=g,
+                            deterministic=det)
 torch.cuda.synchronize()
 rec = tr[1024:].view(n_cta, 8).cpu().tolist()
 t0 = min(r[0] for r in rec)
