@@ -222,3 +222,22 @@ def test_full_mask_64k_chunk_pair(cuda):
     assert rel(_f64(out.o[0, 30000:30128]), o) < TOL
     assert np.abs(_f64(out.lse[0, 30000:30128]) - lse).max() < LSE_TOL
     assert rel(_f64(g.dq[0, 30000:30128]), dq64) < TOL
+
+
+def test_host_pipeline_32k_vs_fp32(cuda):
+    """bench.py's e2e path (the C++ host pipeline: pinned host in, bf16 grads
+    out) at the cfg2 sequence length: dQ/dK/dV of two heads vs the fp32
+    reference (bf16 outputs: the same 2e-2 bar)."""
+    from paper_2310_03294_b200.pipeline import HostAttention
+    h, n = 2, 32768
+    q, k, v, d_out = (_rand((h, n, D), 50 + i) for i in range(4))
+    host_in = [t.cpu().pin_memory() for t in (q, k, v, d_out)]
+    host_out = [torch.empty(h, n, D, dtype=torch.bfloat16).pin_memory() for _ in range(3)]
+    ha = HostAttention(h, n, heads_per_group=2)
+    ha(*host_in, *host_out)
+    o, lse = ha.outputs()
+    o_ref, lse_ref = chunked_attention_fwd(q, k, v, True)
+    assert rel_err(o, o_ref) < TOL and (lse - lse_ref).abs().max().item() < LSE_TOL
+    dq, dk, dv = chunked_attention_bwd(q, k, v, o_ref, lse_ref, d_out, True)
+    for got, ref, name in zip(host_out, (dq, dk, dv), ("dq", "dk", "dv")):
+        assert rel_err(got.cuda(), ref) < TOL, name
