@@ -38,6 +38,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <array>
 #include <cstring>
@@ -247,6 +248,7 @@ struct Nccl {
       nullptr;
   ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*error_string)(ncclResult_t) = nullptr;
+  ncclResult_t (*async_error)(ncclComm_t, ncclResult_t*) = nullptr;
   bool ok = false;
 };
 
@@ -266,6 +268,7 @@ const Nccl& nccl() {
     x.send = reinterpret_cast<decltype(x.send)>(sym("ncclSend"));
     x.recv = reinterpret_cast<decltype(x.recv)>(sym("ncclRecv"));
     x.error_string = reinterpret_cast<decltype(x.error_string)>(sym("ncclGetErrorString"));
+    x.async_error = reinterpret_cast<decltype(x.async_error)>(sym("ncclCommGetAsyncError"));
     x.ok = x.get_unique_id && x.init_rank_config && x.destroy && x.group_start && x.group_end &&
            x.send && x.recv && x.error_string;
     return x;
@@ -336,6 +339,21 @@ da_status nk(ncclResult_t e, const char* where) {
     const da_status s_ = (x);        \
     if (s_ != DA_OK) return s_;      \
   } while (0)
+
+// NCCL's asynchronous errors (a failed peer, a broken connection) surface
+// here after every pass instead of as a silent hang later
+da_status nccl_async_check(da_rank* r) {
+  if (r->comm == nullptr || nccl().async_error == nullptr) return DA_OK;
+  ncclResult_t st = ncclSuccess;
+  DA_TRY(nk(nccl().async_error(r->comm, &st), "ncclCommGetAsyncError"));
+  return nk(st, "NCCL asynchronous error");
+}
+
+// NVTX range for the host-side enqueue of a pass / step (visible in nsys)
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+};
 
 // ---- tracing (no-ops unless da_rank_set_trace enabled it)
 cudaEvent_t trace_event(da_rank* r, cudaStream_t st) {
@@ -727,6 +745,8 @@ static da_status rank_forward_flat(da_rank* r, const FlatSchedule& sch, const vo
                                    const void* k, const void* v, int64_t h_q, int64_t h_kv,
                                    int64_t rows, void* out, float* lse, da_counters* counters,
                                    void* stream) {
+  NvtxScope range("da_rank_forward");
+  DA_TRY(nccl_async_check(r));
   if (h_q < 1 || h_kv < 1 || h_q % h_kv != 0 || rows < 1)
     return set_error(DA_ERR_SHAPE, "da_rank_forward: bad shape");
   const int P = r->world, w = r->rank + 1;
@@ -865,6 +885,7 @@ static da_status rank_forward_flat(da_rank* r, const FlatSchedule& sch, const vo
   r->have_forward = true;
   c.max_remote_chunks_held = held;
   if (counters) *counters = c;
+  DA_TRY(nccl_async_check(r));
   if (r->opts.transport == DA_TRANSPORT_NONE) return DA_OK;  // garbage-in by design
   return da_check_degenerate(r->flag.as<int>(), stream);
 }
@@ -872,6 +893,8 @@ static da_status rank_forward_flat(da_rank* r, const FlatSchedule& sch, const vo
 static da_status rank_backward_flat(da_rank* r, const FlatSchedule& sch, const void* d_out,
                                     float* dq, float* dk, float* dv, da_counters* counters,
                                     void* stream) {
+  NvtxScope range("da_rank_backward");
+  DA_TRY(nccl_async_check(r));
   if (!r->have_forward)
     return set_error(DA_ERR_STATE, "run_backward requires forward output and logsumexp");
   if (d_out == nullptr) return set_error(DA_ERR_STATE, "run_backward requires d_out");
@@ -998,7 +1021,7 @@ static da_status rank_backward_flat(da_rank* r, const FlatSchedule& sch, const v
   }
   if (T >= 1) DA_TRY(complete(T - 1));
   if (counters) *counters = c;
-  return DA_OK;
+  return nccl_async_check(r);
 }
 
 // Re-installs a saved forward state (q, k, v, O, LSE of an earlier forward
