@@ -94,11 +94,19 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
 
 def build_cpp_tests() -> Path:
     """tests/cpp/_build/test_b200_api: the C++ drop-in API (include/distattn/b200.hpp)
-    against the C oracle. Needs libdistattn_b200.so and oracle/liboracle.so."""
+    against the C oracle; tests/cpp/_build/test_rank_cpp: the multi-process
+    RankRuntime driven from C++ only. Needs libdistattn_b200.so and
+    oracle/liboracle.so."""
+    exe = _build_cpp_test("test_b200_api")
+    _build_cpp_test("test_rank_cpp")
+    return exe
+
+
+def _build_cpp_test(name: str) -> Path:
     out_dir = ROOT / "tests" / "cpp" / "_build"
     out_dir.mkdir(parents=True, exist_ok=True)
-    exe = out_dir / "test_b200_api"
-    src = ROOT / "tests" / "cpp" / "test_b200_api.cpp"
+    exe = out_dir / name
+    src = ROOT / "tests" / "cpp" / f"{name}.cpp"
     deps = [src, ROOT / "include" / "distattn" / "b200.hpp", ROOT / "include" / "distattn_b200.h", LIB]
     if exe.exists() and exe.stat().st_mtime >= _newest(deps):
         return exe

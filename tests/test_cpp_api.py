@@ -28,3 +28,20 @@ def test_cpp_api_schedules_cpu():
 def test_cpp_api_kernels_and_runtime(cuda):
     out = _run()
     assert "FAIL" not in out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_cpp_rank_runtime_multiprocess(cuda, world):
+    """tests/cpp/test_rank_cpp.cpp: W forked processes drive
+    distattn::b200::RankRuntime from C++ only (shared-memory allgather
+    bootstrap, IPC transport, split forward + balanced backward, deterministic);
+    each rank's chunk matches the C oracle and a second pass repeats its bits."""
+    exe = EXE.parent / "test_rank_cpp"
+    if not exe.exists():
+        from paper_2310_03294_b200 import build as B
+        B.build_cpp_tests()
+    r = subprocess.run([str(exe), str(world), str(512 * world), "2"], capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "PASS" in r.stdout
