@@ -18,7 +18,8 @@
 // BEFORE the reference's on the include path (errors.hpp, numerics.hpp,
 // schedule.hpp, runtime.hpp ... still come from the reference) and linking
 // libdistattn_b200.so: runtime.cpp and ckptplan.cpp compile unmodified
-// (tests/cpp/dropin_main.cpp builds exactly that).
+// (oracle/Makefile target _ref/dropin_driver builds exactly
+// that from the unmodified reference sources).
 //
 // Precision is the product's (north_star): q/k/v/O/dO are rounded to bf16,
 // the accumulator and statistics to fp32, on upload; results come back as
@@ -43,23 +44,22 @@
 
 namespace distattn {
 
-enum class MaskMode { Diagonal, Full, Empty };
+// Diagonal: query row i sees key rows <= i of the same chunk; Full: every key
+// (an earlier chunk); Empty: none. Values map 1:1 to DA_MASK_*.
+enum class MaskMode { Diagonal = DA_MASK_DIAGONAL, Full = DA_MASK_FULL, Empty = DA_MASK_EMPTY };
 
 inline const char* to_string(MaskMode m) {
-  switch (m) {
-    case MaskMode::Diagonal: return "diagonal";
-    case MaskMode::Full: return "full";
-    case MaskMode::Empty: return "empty";
-  }
-  return "?";
+  static const char* const kNames[] = {"diagonal", "full", "empty"};
+  const int i = static_cast<int>(m);
+  return (i >= 0 && i < 3) ? kNames[i] : "?";
 }
 
+// Accepted and validated for source compatibility; the sm_100a kernels tile
+// by 128 x 128 regardless (score tiles never leave TMEM / shared memory).
 struct BlockConfig {
-  Index rows = 16;
-  Index cols = 16;
-
+  Index rows = 16, cols = 16;
   void check() const {
-    if (rows <= 0 || cols <= 0) throw ConfigError("block sizes must be positive");
+    if (!(rows > 0 && cols > 0)) throw ConfigError("block sizes must be positive");
   }
 };
 
@@ -81,10 +81,21 @@ inline void check_status(da_status s) {
   }
 }
 
-inline int mask_code(MaskMode m) {
-  return m == MaskMode::Diagonal ? DA_MASK_DIAGONAL
-         : m == MaskMode::Full   ? DA_MASK_FULL
-                                 : DA_MASK_EMPTY;
+inline int mask_code(MaskMode m) { return static_cast<int>(m); }
+
+// The reference's operand checks, shared by the update and the backward: the
+// same conditions and messages (op + ": ..."), thrown as ShapeError.
+template <class M>
+inline void check_operands(const char* op, const M& q, const M& k, const M& v) {
+  const std::string o(op);
+  require(q.cols() == k.cols() && k.cols() == v.cols(), o + ": hidden dims disagree");
+  require(k.rows() == v.rows(), o + ": k/v row mismatch");
+}
+
+template <class M>
+inline void check_square(const char* op, MaskMode mask, const M& q, const M& k) {
+  if (mask == MaskMode::Diagonal)
+    require(q.rows() == k.rows(), std::string(op) + ": diagonal mask needs a square chunk");
 }
 
 /// Contiguous double view of an Eigen row-major matrix / vector: the data
@@ -124,18 +135,19 @@ struct HostOut {
 };
 }  // namespace detail
 
+// The running state of one query chunk, in the reference's unnormalised
+// convention: o = sum_j e^{s_j - m} v_j, m = running max, l = sum_j e^{s_j - m}.
 template <class Scalar>
 struct AttnAccumulatorT {
-  Mat<Scalar> o;  // rows x d, unnormalised running output
-  Vec<Scalar> m;  // running row max (natural-log units of scale * q.k)
-  Vec<Scalar> l;  // running row sum
+  Mat<Scalar> o;
+  Vec<Scalar> m;
+  Vec<Scalar> l;
 
+  // the identity of rescale: nothing absorbed yet (m = -inf, l = 0, o = 0)
   static AttnAccumulatorT fresh(Index rows, Index d) {
-    AttnAccumulatorT acc;
-    acc.o = Mat<Scalar>::Zero(rows, d);
-    acc.m = Vec<Scalar>::Constant(rows, -std::numeric_limits<Scalar>::infinity());
-    acc.l = Vec<Scalar>::Zero(rows);
-    return acc;
+    constexpr Scalar kNegInf = -std::numeric_limits<Scalar>::infinity();
+    return AttnAccumulatorT{Mat<Scalar>::Zero(rows, d), Vec<Scalar>::Constant(rows, kNegInf),
+                            Vec<Scalar>::Zero(rows)};
   }
 
   Index rows() const { return o.rows(); }
@@ -156,12 +168,8 @@ using AttnOutput = AttnOutputT<double>;
 template <class Scalar>
 AttnOutputT<Scalar> dense_oracle(const Mat<Scalar>& q, const Mat<Scalar>& k, const Mat<Scalar>& v,
                                  bool causal, Scalar scale) {
-  detail::require(q.cols() == k.cols() && k.cols() == v.cols(),
-                  "dense_oracle: hidden dims disagree");
-  detail::require(k.rows() == v.rows(), "dense_oracle: k/v row mismatch");
-  AttnOutputT<Scalar> out;
-  out.o = Mat<Scalar>::Zero(q.rows(), v.cols());
-  out.lse = Vec<Scalar>(q.rows());
+  detail::check_operands("dense_oracle", q, k, v);
+  AttnOutputT<Scalar> out{Mat<Scalar>::Zero(q.rows(), v.cols()), Vec<Scalar>(q.rows())};
   detail::HostIn<Scalar, Mat<Scalar>> hq(q), hk(k), hv(v);
   {
     detail::HostOut<Scalar, Mat<Scalar>> ho(out.o);
@@ -180,14 +188,11 @@ AttnAccumulatorT<Scalar> block_attn_update(const Mat<Scalar>& q, const Mat<Scala
                                            const Mat<Scalar>& v, AttnAccumulatorT<Scalar> acc,
                                            MaskMode mask, Scalar scale, BlockConfig blocks = {}) {
   blocks.check();
-  detail::require(q.cols() == k.cols() && k.cols() == v.cols(),
-                  "block_attn_update: hidden dims disagree");
-  detail::require(k.rows() == v.rows(), "block_attn_update: k/v row mismatch");
+  detail::check_operands("block_attn_update", q, k, v);
   detail::require(acc.rows() == q.rows() && acc.dim() == q.cols(),
                   "block_attn_update: accumulator shape mismatch");
-  if (mask == MaskMode::Empty) return acc;
-  if (mask == MaskMode::Diagonal)
-    detail::require(q.rows() == k.rows(), "block_attn_update: diagonal mask needs a square chunk");
+  if (mask == MaskMode::Empty) return acc;  // bit-identical no-op
+  detail::check_square("block_attn_update", mask, q, k);
   detail::HostIn<Scalar, Mat<Scalar>> hq(q), hk(k), hv(v);
   {
     detail::HostOut<Scalar, Mat<Scalar>> ho(acc.o);
@@ -265,22 +270,17 @@ ChunkGradsT<Scalar> block_attn_backward(const Mat<Scalar>& q, const Mat<Scalar>&
                                         const Vec<Scalar>& lse, const Mat<Scalar>& d_out,
                                         MaskMode mask, Scalar scale, BlockConfig blocks = {}) {
   blocks.check();
-  detail::require(q.cols() == k.cols() && k.cols() == v.cols(),
-                  "block_attn_backward: hidden dims disagree");
-  detail::require(k.rows() == v.rows(), "block_attn_backward: k/v row mismatch");
-  detail::require(out.rows() == q.rows() && out.cols() == q.cols(),
-                  "block_attn_backward: output shape mismatch");
-  detail::require(d_out.rows() == q.rows() && d_out.cols() == q.cols(),
-                  "block_attn_backward: upstream grad shape mismatch");
+  detail::check_operands("block_attn_backward", q, k, v);
+  const auto same_as_q = [&](const Mat<Scalar>& x) {
+    return x.rows() == q.rows() && x.cols() == q.cols();
+  };
+  detail::require(same_as_q(out), "block_attn_backward: output shape mismatch");
+  detail::require(same_as_q(d_out), "block_attn_backward: upstream grad shape mismatch");
   detail::require(lse.size() == q.rows(), "block_attn_backward: logsumexp length mismatch");
-  if (mask == MaskMode::Diagonal)
-    detail::require(q.rows() == k.rows(),
-                    "block_attn_backward: diagonal mask needs a square chunk");
-  ChunkGradsT<Scalar> g;
-  g.dq = Mat<Scalar>::Zero(q.rows(), q.cols());
-  g.dk = Mat<Scalar>::Zero(k.rows(), k.cols());
-  g.dv = Mat<Scalar>::Zero(v.rows(), v.cols());
-  if (mask == MaskMode::Empty) return g;
+  detail::check_square("block_attn_backward", mask, q, k);
+  ChunkGradsT<Scalar> g{Mat<Scalar>::Zero(q.rows(), q.cols()), Mat<Scalar>::Zero(k.rows(), k.cols()),
+                        Mat<Scalar>::Zero(v.rows(), v.cols())};
+  if (mask == MaskMode::Empty) return g;  // zero contribution
   detail::HostIn<Scalar, Mat<Scalar>> hq(q), hk(k), hv(v), ho(out), hdo(d_out);
   detail::HostIn<Scalar, Vec<Scalar>> hl(lse);
   {
