@@ -27,7 +27,8 @@ NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr", "-Xc
 
 
 # kernels that redistribute registers with setmaxnreg need a known launch budget
-PER_FILE = {"attn_bwd_ws_sm100.cu": ["-maxrregcount=128"]}
+PER_FILE = {"attn_bwd_ws_sm100.cu": ["-maxrregcount=128"],
+            "attn_bwd_pair_sm100.cu": ["-maxrregcount=128"]}
 
 
 def nvcc() -> str:

@@ -49,13 +49,14 @@ da_status cuda_error(cudaError_t e, const char* where) {
 
 const char* last_error() { return g_last_error.c_str(); }
 
-// bf16 [heads][rows][128] tensor -> 3D tensor map, box {64, 128, 1}, SWIZZLE_128B.
-da_status make_tmap_3d(CUtensorMap* map, const void* base, int64_t heads, int64_t rows) {
+// bf16 [heads][rows][128] tensor -> 3D tensor map, box {64, box_rows, 1}, SWIZZLE_128B.
+da_status make_tmap_3d(CUtensorMap* map, const void* base, int64_t heads, int64_t rows,
+                       uint32_t box_rows) {
   EncodeTiledFn fn = encode_fn();
   if (fn == nullptr) return set_error(DA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[3] = {128, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(heads)};
   const cuuint64_t strides[2] = {128 * 2, static_cast<cuuint64_t>(rows) * 128 * 2};
-  const cuuint32_t box[3] = {64, 128, 1};
+  const cuuint32_t box[3] = {64, box_rows, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -65,7 +66,8 @@ da_status make_tmap_3d(CUtensorMap* map, const void* base, int64_t heads, int64_
   return DA_OK;
 }
 
-da_status make_tmap_f32_acc(CUtensorMap* map, void* base, int64_t heads, int64_t rows) {
+da_status make_tmap_f32_acc(CUtensorMap* map, void* base, int64_t heads, int64_t rows,
+                            bool swizzle128) {
   EncodeTiledFn fn = encode_fn();
   if (fn == nullptr) return set_error(DA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[3] = {128, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(heads)};
@@ -73,7 +75,8 @@ da_status make_tmap_f32_acc(CUtensorMap* map, void* base, int64_t heads, int64_t
   const cuuint32_t box[3] = {32, 32, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return set_error(DA_ERR_CUDA, "cuTensorMapEncodeTiled(f32) failed (" + std::to_string(r) + ")");
@@ -286,7 +289,6 @@ da_status da_attn_bwd_chunk(const da_bwd_args* a, void* stream) {
   if ((s = da::make_tmap_3d(&tk, a->k, a->h_kv, a->rows_kv)) != DA_OK) return s;
   if ((s = da::make_tmap_3d(&tv, a->v, a->h_kv, a->rows_kv)) != DA_OK) return s;
   if ((s = da::make_tmap_3d(&tdo, a->d_out, a->h_q, a->rows_q)) != DA_OK) return s;
-  if ((s = da::make_tmap_f32_acc(&tdq, a->dq_acc, a->h_q, a->rows_q)) != DA_OK) return s;
   da::BwdParams p{};
   p.h_q = static_cast<int>(a->h_q);
   p.h_kv = static_cast<int>(a->h_kv);
@@ -310,7 +312,19 @@ da_status da_attn_bwd_chunk(const da_bwd_args* a, void* stream) {
     p.dq_sem = sem;
   }
   p.trace = da::g_bwd_trace;
-  cudaError_t e = da::launch_attn_bwd(tq, tk, tv, tdo, tdq, p, st);
+  cudaError_t e;
+  if (p.dq_sem == nullptr && da::bwd_pair_enabled()) {
+    // CTA-pair kernel (attn_bwd_pair_sm100.cu); the deterministic dQ order
+    // lives in the single-CTA kernel
+    CUtensorMap tq64, tdo64;
+    if ((s = da::make_tmap_3d(&tq64, a->q, a->h_q, a->rows_q, 64)) != DA_OK) return s;
+    if ((s = da::make_tmap_3d(&tdo64, a->d_out, a->h_q, a->rows_q, 64)) != DA_OK) return s;
+    if ((s = da::make_tmap_f32_acc(&tdq, a->dq_acc, a->h_q, a->rows_q, true)) != DA_OK) return s;
+    e = da::launch_attn_bwd_pair(tq, tq64, tk, tv, tdo, tdo64, tdq, p, st);
+  } else {
+    if ((s = da::make_tmap_f32_acc(&tdq, a->dq_acc, a->h_q, a->rows_q, false)) != DA_OK) return s;
+    e = da::launch_attn_bwd(tq, tk, tv, tdo, tdq, p, st);
+  }
   return e == cudaSuccess ? DA_OK : da::cuda_error(e, "da_attn_bwd_chunk launch");
 }
 

@@ -66,6 +66,19 @@ cudaError_t launch_attn_bwd(const CUtensorMap& tq, const CUtensorMap& tk, const 
                             const CUtensorMap& tdo, const CUtensorMap& tdq, const BwdParams& p,
                             cudaStream_t stream);
 
+// CTA-pair backward (attn_bwd_pair_sm100.cu): q64/do64 are 64-row-box maps of
+// q / d_out, tdq_sw the 128B-swizzled fp32 dq_acc map. Not deterministic.
+cudaError_t launch_attn_bwd_pair(const CUtensorMap& tq, const CUtensorMap& tq64,
+                                 const CUtensorMap& tk, const CUtensorMap& tv,
+                                 const CUtensorMap& tdo, const CUtensorMap& tdo64,
+                                 const CUtensorMap& tdq_sw, const BwdParams& p,
+                                 cudaStream_t stream);
+// whether the non-deterministic backward uses the CTA-pair kernel: only with
+// DA_BWD_KERNEL=pair (read once per process). The pair kernel is correct but
+// measured slower than the single-CTA kernel, so it is an
+// opt-in experiment, not the product default.
+bool bwd_pair_enabled();
+
 cudaError_t launch_merge(const float* o_a, const float* m_a, const float* l_a, const float* o_b,
                          const float* m_b, const float* l_b, float* o_out, float* m_out,
                          float* l_out, int64_t rows_total, cudaStream_t stream);
