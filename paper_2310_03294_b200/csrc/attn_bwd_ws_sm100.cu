@@ -626,12 +626,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float2 t23 =
               fadd2(make_float2(__uint_as_float(dr[i + 2]), __uint_as_float(dr[i + 3])),
                     make_float2(d4.z, d4.w));
-          const float2 s01 =
-              fmul2(make_float2(__uint_as_float(a << 16), __uint_as_float(a & 0xFFFF0000u)), t01);
-          const float2 s23 =
-              fmul2(make_float2(__uint_as_float(b << 16), __uint_as_float(b & 0xFFFF0000u)), t23);
-          dsk[i / 2] = pack_bf16x2(s01.x, s01.y);
-          dsk[i / 2 + 1] = pack_bf16x2(s23.x, s23.y);
+          // dS = P o bf16(dP - D) as one packed bf16 multiply per column pair:
+          // the subtraction stays fp32 (no cancellation loss); dS is a bf16 MMA
+          // operand either way. Against unpacking P and an fp32 multiply this
+          // drops 3 of 5 instructions per pair on the dS warps (the cycle's
+          // critical phase): backward -2.5% time, max rel. error of dq/dk
+          // ~1.3x higher (e.g. dk 4.3e-3 -> 5.5e-3 at 4 x 4K; bar 2e-2),
+          // profiles/ab_r2_bwd_ds_bf16mul.txt
+          dsk[i / 2] = mul_bf16x2(a, pack_bf16x2(t01.x, t01.y));
+          dsk[i / 2 + 1] = mul_bf16x2(b, pack_bf16x2(t23.x, t23.y));
         }
         // dS^T packed into the (already read) low columns of the dP region ...
         tmem_st_32x32b_x16(dp_tmem + c * 16, dsk);

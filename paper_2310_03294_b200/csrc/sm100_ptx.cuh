@@ -398,6 +398,13 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return r;
 }
 
+// packed bf16x2 product (round to nearest)
+__device__ __forceinline__ uint32_t mul_bf16x2(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("mul.rn.bf16x2 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
 // bf16x2 pack on the integer pipes (IADD + PRMT) instead of F2FP: rounds
 // half away from zero in magnitude (+0x8000, truncate) -- for finite values
 // whose bf16 rounding does not overflow (probabilities in [0, 1]).
