@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (row < p.rows_q) {
           const size_t idx = static_cast<size_t>(hq) * p.rows_q + row;
           l2[k] = -p.lse[idx] * kLog2e;
-          dd[k] = -p.d_vec[idx];
+          dd[k] = -p.d_vec[idx] * p.scale;  // the softmax scale rides on dS
         }
       }
       if (lane == 0) {
@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) bulk_wait_read<1>();
         __syncwarp();
 #pragma unroll
-        for (int k = 0; k < 32; ++k) box[k * 32 + lane] = p.scale * __uint_as_float(r[c][k]);
+        for (int k = 0; k < 32; ++k) box[k * 32 + lane] = __uint_as_float(r[c][k]);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -575,6 +575,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t s_tmem = lane_base + kColS;
     const uint32_t dp_tmem = lane_base + kColDP;
     uint8_t* ds_row = smem + SmemLayout::ds + r * 128;
+    const float2 sc2 = make_float2(p.scale, p.scale);
     ItCursor cur = cur0;
     for (int it = 0; it < n_it; ++it, cur.next()) {
       const int st = it & 1;
@@ -614,17 +615,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           float dv4[4];
           for (int u = 0; u < 4; ++u) {
             const int row = cur.qt * kBM + qc + u;
-            dv4[u] = row < p.rows_q ? -p.d_vec[static_cast<size_t>(cur.hq) * p.rows_q + row] : 0.f;
+            dv4[u] = row < p.rows_q ? -p.d_vec[static_cast<size_t>(cur.hq) * p.rows_q + row] * p.scale : 0.f;
           }
           const float4 d4 = make_float4(dv4[0], dv4[1], dv4[2], dv4[3]);
 #else
           const float4 d4 = *reinterpret_cast<const float4*>(dvec + qc);
 #endif
           const uint32_t a = pk[qc >> 6][(qc & 63) / 2], b = pk[qc >> 6][(qc & 63) / 2 + 1];
-          const float2 t01 = fadd2(make_float2(__uint_as_float(dr[i]), __uint_as_float(dr[i + 1])),
-                                   make_float2(d4.x, d4.y));
+          // t = scale (dP - D) = scale dP + (-scale D): dS, hence dQ and dK, come
+          // out scaled, so neither the dQ drain nor the dK epilogue multiplies
+          const float2 t01 = ffma2(make_float2(__uint_as_float(dr[i]), __uint_as_float(dr[i + 1])),
+                                   sc2, make_float2(d4.x, d4.y));
           const float2 t23 =
-              fadd2(make_float2(__uint_as_float(dr[i + 2]), __uint_as_float(dr[i + 3])),
+              ffma2(make_float2(__uint_as_float(dr[i + 2]), __uint_as_float(dr[i + 3])), sc2,
                     make_float2(d4.z, d4.w));
           // dS = P o bf16(dP - D) as one packed bf16 multiply per column pair:
           // the subtraction stays fp32 (no cancellation loss); dS is a bf16 MMA
@@ -660,7 +663,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&bars->acc_full, 0);
       tc_fence_after();
       store_acc_rows_lsu(p.dk_acc + (static_cast<size_t>(kv_head) * p.rows_kv + jt * kBN + r) * kHD,
-                         jt * kBN + r < p.rows_kv, lane_base + kColDK, p.scale, p.accumulate_kv != 0);
+                         jt * kBN + r < p.rows_kv, lane_base + kColDK, 1.f, p.accumulate_kv != 0);
     } else if (p.mask != DA_MASK_EMPTY && !p.accumulate_kv) {
       const int row = jt * kBN + r;
       if (row < p.rows_kv) {
