@@ -213,7 +213,14 @@ da_status da_attn_fwd_chunk(const da_fwd_args* a, void* stream) {
   p.degenerate_flag = a->degenerate_flag;
   p.debug_s = nullptr;
   p.trace = da::g_fwd_trace;
-  cudaError_t e = da::launch_attn_fwd(tq, tk, tv, p, st);
+  cudaError_t e;
+  if (da::fwd_pair_enabled()) {
+    CUtensorMap tk64;
+    if ((s = da::make_tmap_3d(&tk64, a->k, a->h_kv, a->rows_kv, 64)) != DA_OK) return s;
+    e = da::launch_attn_fwd_pair(tq, tk64, tv, p, st);
+  } else {
+    e = da::launch_attn_fwd(tq, tk, tv, p, st);
+  }
   return e == cudaSuccess ? DA_OK : da::cuda_error(e, "da_attn_fwd_chunk launch");
 }
 

@@ -62,6 +62,12 @@ struct BwdParams {
 cudaError_t launch_attn_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                             const FwdParams& p, cudaStream_t stream);
 
+// CTA-pair forward (attn_fwd_pair_sm100.cu): tk64 is a 64-row-box map of k.
+cudaError_t launch_attn_fwd_pair(const CUtensorMap& tq, const CUtensorMap& tk64,
+                                 const CUtensorMap& tv, const FwdParams& p, cudaStream_t stream);
+// whether the forward uses the CTA-pair kernel (DA_FWD_KERNEL=pair, read once per process)
+bool fwd_pair_enabled();
+
 cudaError_t launch_attn_bwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                             const CUtensorMap& tdo, const CUtensorMap& tdq, const BwdParams& p,
                             cudaStream_t stream);
