@@ -726,7 +726,8 @@ def main(argv=None):
     ap.add_argument("--heads-per-group", type=int, default=2)  # e2e copy/compute granularity (A/B: 2 >= 1 by ~0.5-1%)
     ap.add_argument("--fwd-schedule", default="balanced_split",
                     choices=["ring", "balanced", "balanced_split"])
-    ap.add_argument("--bwd-schedule", default="balanced", choices=["ring", "balanced"])
+    ap.add_argument("--bwd-schedule", default="balanced_split",
+                    choices=["ring", "balanced", "balanced_split"])
     ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "ipc"],
                     help="N>1: NCCL send/recv (distinct GPUs) or CUDA-IPC pulls (shared GPU)")
     ap.add_argument("--nccl-max-ctas", type=int, default=0)

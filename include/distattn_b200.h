@@ -244,7 +244,14 @@ typedef enum da_schedule_kind {
    * RemoteAttn tasks the `helper` slot carries the kv row part:
    * 0 whole chunk, 1 rows [0, c/2), 2 rows [c/2, c). The owner's half arrives
    * as message kind 4 (KVHalf). Odd P: identical to DA_SCHEDULE_BALANCED. */
-  DA_SCHEDULE_BALANCED_SPLIT = 4
+  DA_SCHEDULE_BALANCED_SPLIT = 4,
+  /* Backward of the split schedule (extension): the DA_SCHEDULE_BALANCED_SPLIT
+   * task table with the backward messages of BALANCED_BWD. At t = P/2 the
+   * owner computes its pair on the high half of the kv rows (KVHalf in, the
+   * half's GradKV back to the kv owner) and the helper on the low half (the
+   * Q bundle in, the dq Partial back); the helper keeps its low half's dk/dv.
+   * Odd P: identical to DA_SCHEDULE_BALANCED_BWD. */
+  DA_SCHEDULE_BALANCED_SPLIT_BWD = 5
 } da_schedule_kind;
 
 da_status da_schedule_build(int workers, int kind, int32_t* steps_out, int32_t* tasks,

@@ -559,6 +559,8 @@ int dao_run_backward_sched(int P, int kind, int64_t n, int64_t d, const double* 
   double* pv = (double*)malloc(sizeof(double) * osz * (size_t)P);
   double* pq = (double*)malloc(sizeof(double) * osz * (size_t)P);
   int* gk_to = (int*)malloc(sizeof(int) * (size_t)P); /* receiver of sender's GradKV, 0 = none */
+  int64_t* gk_r0 = (int64_t*)malloc(sizeof(int64_t) * (size_t)P); /* its kv row window */
+  int64_t* gk_nr = (int64_t*)malloc(sizeof(int64_t) * (size_t)P);
   int64_t c[10] = {0};
   for (int t = 0; t < steps; ++t) {
     for (int w = 0; w < P; ++w) gk_to[w] = 0;
@@ -578,26 +580,36 @@ int dao_run_backward_sched(int P, int kind, int64_t n, int64_t d, const double* 
         }
       } else if (tk[2] == tk[3]) { /* direct */
         const int r = tk[4];
-        const size_t ro = (size_t)(r - 1) * osz;
-        count_msg(c, 0, rows, d);
+        /* kv row window: whole chunk, or the low/high half of the split step */
+        const int64_t lo = rows / 2;
+        const int64_t r0 = tk[5] == 2 ? lo : 0;
+        const int64_t nr = tk[5] == 0 ? rows : (tk[5] == 1 ? lo : rows - lo);
+        const size_t ro = (size_t)(r - 1) * osz + (size_t)(r0 * d);
+        count_msg(c, tk[5] == 0 ? 0 : 4, nr, d);
         c[9] = 1;
-        dao_block_attn_backward(q + wo, rows, k + ro, v + ro, rows, d, out + wo,
+        dao_block_attn_backward(q + wo, rows, k + ro, v + ro, nr, d, out + wo,
                                 lse + (w - 1) * rows, d_out + wo, 1, scale, 16, 16, gq, pk + wo,
                                 pv + wo);
         gk_to[w - 1] = r;
+        gk_r0[w - 1] = r0;
+        gk_nr[w - 1] = nr;
         for (size_t x = 0; x < osz; ++x) dq[wo + x] += gq[x];
-      } else { /* helper w for owner o on its own kv */
+      } else { /* helper w for owner o on (a row window of) its own kv */
         const int o = tk[3];
         const size_t oo = (size_t)(o - 1) * osz;
+        const int64_t lo = rows / 2;
+        const int64_t r0 = tk[5] == 2 ? lo : 0;
+        const int64_t nr = tk[5] == 0 ? rows : (tk[5] == 1 ? lo : rows - lo);
+        const size_t wk = wo + (size_t)(r0 * d);
         c[1] += rows * (2 * d + 2);
         ++c[5];
         c[9] = 1;
-        dao_block_attn_backward(q + oo, rows, k + wo, v + wo, rows, d, out + oo,
+        dao_block_attn_backward(q + oo, rows, k + wk, v + wk, nr, d, out + oo,
                                 lse + (o - 1) * rows, d_out + oo, 1, scale, 16, 16, pq + wo, gk,
                                 gv);
-        for (size_t x = 0; x < osz; ++x) {
-          dk[wo + x] += gk[x];
-          dv[wo + x] += gv[x];
+        for (size_t x = 0; x < (size_t)(nr * d); ++x) {
+          dk[wk + x] += gk[x];
+          dv[wk + x] += gv[x];
         }
       }
     }
@@ -605,9 +617,10 @@ int dao_run_backward_sched(int P, int kind, int64_t n, int64_t d, const double* 
     for (int r = 1; r <= P; ++r)
       for (int s = 1; s <= P; ++s)
         if (gk_to[s - 1] == r) {
-          count_msg(c, 3, rows, d);
-          const size_t ro = (size_t)(r - 1) * osz, so = (size_t)(s - 1) * osz;
-          for (size_t x = 0; x < osz; ++x) {
+          count_msg(c, 3, gk_nr[s - 1], d);
+          const size_t ro = (size_t)(r - 1) * osz + (size_t)(gk_r0[s - 1] * d);
+          const size_t so = (size_t)(s - 1) * osz;
+          for (size_t x = 0; x < (size_t)(gk_nr[s - 1] * d); ++x) {
             dk[ro + x] += pk[so + x];
             dv[ro + x] += pv[so + x];
           }
@@ -625,6 +638,7 @@ int dao_run_backward_sched(int P, int kind, int64_t n, int64_t d, const double* 
   }
   if (counters) memcpy(counters, c, sizeof(c));
   free(tasks); free(msgs); free(gq); free(gk); free(gv); free(pk); free(pv); free(pq); free(gk_to);
+  free(gk_r0); free(gk_nr);
   return 0;
 }
 

@@ -234,13 +234,15 @@ def run_backward(q, k, v, out, lse, d_out, workers: int):
 
 
 def run_backward_sched(q, k, v, out, lse, d_out, workers: int, schedule: str):
-    """Backward over the ring or balanced backward schedule (balanced: extension)."""
+    """Backward over the ring, balanced or balanced_split backward schedule
+    (balanced / balanced_split: extensions; the task table of run_forward's
+    schedule of that name plus a GradKV per direct task)."""
     q, k, v, out, lse, d_out = (np.ascontiguousarray(x, dtype=np.float64)
                                 for x in (q, k, v, out, lse, d_out))
     n, d = q.shape
     dq, dk, dv = np.empty((n, d)), np.empty((n, d)), np.empty((n, d))
     c = (C.c_int64 * 10)()
-    _ok(lib().dao_run_backward_sched(workers, 0 if schedule == "ring" else 1, n, d, q, k, v, out,
+    _ok(lib().dao_run_backward_sched(workers, _KINDS[schedule], n, d, q, k, v, out,
                                      lse, d_out, dq, dk, dv, c), "run_backward_sched")
     return dq, dk, dv, list(c)
 

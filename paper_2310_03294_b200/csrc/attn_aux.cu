@@ -185,6 +185,38 @@ cudaError_t launch_add(float* dst, const float* src, int64_t n, cudaStream_t str
   return cudaGetLastError();
 }
 
+// dst[h][r0 + i][:] += src[h][i][:] for i < n (fp32 rows of 128): the fold of a
+// kv row half (split schedules) into a [h, rows_dst, 128] accumulator
+__global__ void add_rows_kernel(float4* __restrict__ dst, const float4* __restrict__ src,
+                                int64_t rows_dst, int64_t r0, int64_t n, int64_t total4) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total4;
+       i += stride) {
+    const int64_t row = i / 32, c4 = i % 32;  // 32 float4 per 128-wide row
+    const int64_t h = row / n, r = row % n;
+    float4* d = dst + ((h * rows_dst + r0 + r) * 32 + c4);
+    const float4 b = src[i];
+    float4 a = *d;
+    a.x += b.x;
+    a.y += b.y;
+    a.z += b.z;
+    a.w += b.w;
+    *d = a;
+  }
+}
+
+cudaError_t launch_add_rows(float* dst, const float* src, int64_t h, int64_t rows_dst, int64_t r0,
+                            int64_t n, cudaStream_t stream) {
+  if (h <= 0 || n <= 0) return cudaSuccess;
+  const int64_t total4 = h * n * 32;
+  const int64_t blocks = (total4 + 255) / 256;
+  const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
+  add_rows_kernel<<<static_cast<unsigned>(blocks < cap ? blocks : cap), 256, 0, stream>>>(
+      reinterpret_cast<float4*>(dst), reinterpret_cast<const float4*>(src), rows_dst, r0, n,
+      total4);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_convert(const float* src, void* dst, int64_t n, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
   const int64_t n4 = n / 4;

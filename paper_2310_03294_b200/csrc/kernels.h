@@ -99,6 +99,10 @@ cudaError_t launch_convert(const float* src, void* dst, int64_t n, cudaStream_t 
 
 cudaError_t launch_add(float* dst, const float* src, int64_t n, cudaStream_t stream);
 
+// dst[h][r0 + i][:] += src[h][i][:], i < n: fp32 [h, rows_dst, 128] += [h, n, 128]
+cudaError_t launch_add_rows(float* dst, const float* src, int64_t h, int64_t rows_dst, int64_t r0,
+                            int64_t n, cudaStream_t stream);
+
 cudaError_t launch_copy_acc(const float* o, const float* m, const float* l, float* o_out,
                             float* m_out, float* l_out, int64_t rows_total, cudaStream_t stream);
 

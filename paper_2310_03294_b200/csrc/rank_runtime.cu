@@ -62,11 +62,14 @@ namespace {
 enum Key : int {
   kK = 0, kV, kQ, kPart, kKHi, kVHi,                    // forward
   kDOut, kLse, kDVec, kGK0, kGV0, kGK1, kGV1, kGQ0, kGQ1,  // backward
+  kGKH, kGVH,                                              // backward split step: a half's GradKV
   kNumKeys
 };
 
 // receive slots (resolved to device addresses by the executor)
-enum Slot : int { kSlotKV = 0, kSlotKVH, kSlotQ, kSlotPart, kSlotBundle, kSlotGrad, kSlotGQ };
+enum Slot : int {
+  kSlotKV = 0, kSlotKVH, kSlotQ, kSlotPart, kSlotBundle, kSlotGrad, kSlotGQ, kSlotGradH
+};
 
 struct XSend {
   int dst;  // 0-based rank
@@ -89,6 +92,7 @@ struct Plan {
   int action = 0;  // 0 idle, 1 local, 2 direct, 3 help
   int peer = 0;    // 1-based
   int part = kPartWhole;
+  int gradkv_part = kPartWhole;  // backward: row part of the GradKV this worker receives
   std::vector<int> kv_sends, kvh_sends, q_sends, merges, gradkv_from, gradkv_to;
 };
 
@@ -112,10 +116,26 @@ std::vector<Plan> plans_for(const FlatSchedule& s, int worker) {
     if (m.from == worker && m.kind == kMsgKV) p.kv_sends.push_back(m.to);
     if (m.from == worker && m.kind == kMsgKVHalf) p.kvh_sends.push_back(m.to);
     if (m.from == worker && m.kind == kMsgQ) p.q_sends.push_back(m.to);
-    if (m.to == worker && m.kind == kMsgGradKV) p.gradkv_from.push_back(m.from);
+    if (m.to == worker && m.kind == kMsgGradKV) {
+      p.gradkv_from.push_back(m.from);
+      for (const Task& k : s.tasks)  // the sender's direct task of that step: its row part
+        if (k.step == m.step && k.kind == kRemote && k.worker == m.from && k.query_owner == m.from)
+          p.gradkv_part = k.helper;
+    }
     if (m.from == worker && m.kind == kMsgGradKV) p.gradkv_to.push_back(m.to);
   }
   return plans;
+}
+
+// Split steps as the executors implement them (make_balanced_split): a direct
+// task takes the high half of the kv rows (KVHalf payload), a helper the low
+// half of its own rows.
+da_status check_parts(const std::vector<Plan>& plans) {
+  for (const Plan& p : plans)
+    if ((p.action == 2 && p.part == kPartLow) || (p.action == 3 && p.part == kPartHigh))
+      return set_error(DA_ERR_UNSUPPORTED,
+                       "split step: direct tasks take the high half, helpers the low half");
+  return DA_OK;
 }
 
 // The pass as phases: [operands(0)], then per step t: operands(t+1), results(t).
@@ -128,6 +148,7 @@ struct Program {
 da_status forward_program(const FlatSchedule& s, int worker, Program* out) {
   Program pg;
   pg.plans = plans_for(s, worker);
+  if (check_parts(pg.plans) != DA_OK) return DA_ERR_UNSUPPORTED;
   const int T = static_cast<int>(pg.plans.size());
   pg.operands.resize(T);
   pg.results.resize(T);
@@ -158,6 +179,7 @@ da_status forward_program(const FlatSchedule& s, int worker, Program* out) {
 da_status backward_program(const FlatSchedule& s, int worker, Program* out) {
   Program pg;
   pg.plans = plans_for(s, worker);
+  if (check_parts(pg.plans) != DA_OK) return DA_ERR_UNSUPPORTED;
   const int T = static_cast<int>(pg.plans.size());
   pg.operands.resize(T);
   pg.results.resize(T);
@@ -173,10 +195,15 @@ da_status backward_program(const FlatSchedule& s, int worker, Program* out) {
       return set_error(DA_ERR_SCHEDULE, "at most one GradKV per worker and step is supported");
     Phase& op = pg.operands[t];
     for (int dst : p.kv_sends) op.sends.insert(op.sends.end(), {{dst - 1, kK}, {dst - 1, kV}});
+    for (int dst : p.kvh_sends)
+      op.sends.insert(op.sends.end(), {{dst - 1, kKHi}, {dst - 1, kVHi}});
     for (int dst : p.q_sends)
       op.sends.insert(op.sends.end(),
                       {{dst - 1, kQ}, {dst - 1, kDOut}, {dst - 1, kLse}, {dst - 1, kDVec}});
-    if (p.action == 2) {
+    if (p.action == 2 && p.part == kPartHigh) {
+      op.recvs.push_back({p.peer - 1, kKHi, kSlotKVH, 0, 0});
+      op.recvs.push_back({p.peer - 1, kVHi, kSlotKVH, 0, 1});
+    } else if (p.action == 2) {
       op.recvs.push_back({p.peer - 1, kK, kSlotKV, t % 2, 0});
       op.recvs.push_back({p.peer - 1, kV, kSlotKV, t % 2, 1});
     } else if (p.action == 3) {
@@ -188,13 +215,21 @@ da_status backward_program(const FlatSchedule& s, int worker, Program* out) {
     Phase& res = pg.results[t];
     const Key gk = (t % 2) ? kGK1 : kGK0, gv = (t % 2) ? kGV1 : kGV0;
     const Key gq = (t % 2) ? kGQ1 : kGQ0;
-    if (p.action == 2) res.sends.insert(res.sends.end(), {{p.peer - 1, gk}, {p.peer - 1, gv}});
+    if (p.action == 2 && p.part == kPartHigh)
+      res.sends.insert(res.sends.end(), {{p.peer - 1, kGKH}, {p.peer - 1, kGVH}});
+    else if (p.action == 2)
+      res.sends.insert(res.sends.end(), {{p.peer - 1, gk}, {p.peer - 1, gv}});
     if (p.action == 3) res.sends.push_back({p.peer - 1, gq});
     // receive slots alternate by step parity: results(t) are folded during
     // step t+1 (after its kernel is queued), while results(t+1) may land
     for (int src : p.gradkv_from) {
-      res.recvs.push_back({src - 1, gk, kSlotGrad, t % 2, 0});
-      res.recvs.push_back({src - 1, gv, kSlotGrad, t % 2, 1});
+      if (p.gradkv_part == kPartHigh) {  // the split step's half: one slot (one such step)
+        res.recvs.push_back({src - 1, kGKH, kSlotGradH, 0, 0});
+        res.recvs.push_back({src - 1, kGVH, kSlotGradH, 0, 1});
+      } else {
+        res.recvs.push_back({src - 1, gk, kSlotGrad, t % 2, 0});
+        res.recvs.push_back({src - 1, gv, kSlotGrad, t % 2, 1});
+      }
     }
     for (int hw : p.merges) res.recvs.push_back({hw - 1, gq, kSlotGQ, 2 * hw + t % 2, 0});
   }
@@ -320,6 +355,7 @@ struct da_rank {
   da::Buf acc, part, kv_slot[2], q_slot[2], k_lo, v_lo, k_hi, v_hi, kvh, flag;
   std::map<int, da::Buf> part_recv, gq_recv;
   da::Buf d_vec, bundle[2], g_send[2], q_send[2], g_recv[2];
+  da::Buf gh_send, gh_recv, dkv_lo;  // split backward: a half's dk | dv (send / receive), low half's
 };
 
 namespace da {
@@ -571,7 +607,7 @@ da_status fwd_chunk(const void* q, const void* k, const void* v, int64_t h_q, in
 
 da_status bwd_chunk(const void* q, const void* k, const void* v, const void* d_out,
                     const float* lse, const float* d_vec, int64_t h_q, int64_t h_kv, int64_t rows,
-                    float* dq, float* dk, float* dv, bool accumulate_kv, int mask,
+                    int64_t rows_kv, float* dq, float* dk, float* dv, bool accumulate_kv, int mask,
                     bool deterministic, cudaStream_t st) {
   da_bwd_args a{};
   a.q = q;
@@ -583,7 +619,7 @@ da_status bwd_chunk(const void* q, const void* k, const void* v, const void* d_o
   a.h_q = h_q;
   a.h_kv = h_kv;
   a.rows_q = rows;
-  a.rows_kv = rows;
+  a.rows_kv = rows_kv;
   a.d = 128;
   a.dq_acc = dq;
   a.dk_acc = dk;
@@ -624,6 +660,8 @@ FlatSchedule backward_table(int kind, int P, bool* ok) {
   if (kind == DA_SCHEDULE_RING_BWD || kind == DA_SCHEDULE_RING) return make_ring_backward(P);
   if (kind == DA_SCHEDULE_BALANCED_BWD || kind == DA_SCHEDULE_BALANCED)
     return make_balanced_backward(P);
+  if (kind == DA_SCHEDULE_BALANCED_SPLIT_BWD || kind == DA_SCHEDULE_BALANCED_SPLIT)
+    return make_balanced_split_backward(P);
   *ok = false;
   return FlatSchedule{};
 }
@@ -651,6 +689,8 @@ void* bwd_slot(da_rank* r, const XRecv& x) {
     case kSlotBundle: return r->bundle[x.index].as<char>() + bundle_off[x.part];
     case kSlotGrad: return r->g_recv[x.index].as<char>() + x.part * g_kv;
     case kSlotGQ: return r->gq_recv[x.index].p;
+    case kSlotKVH: return r->kvh.as<char>() + x.part * r->key_bytes[kKHi];
+    case kSlotGradH: return r->gh_recv.as<char>() + x.part * r->key_bytes[kGKH];
     default: return nullptr;
   }
 }
@@ -924,6 +964,32 @@ static da_status rank_backward_flat(da_rank* r, const FlatSchedule& sch, const v
   for (size_t t = 0; t < plans.size(); ++t)
     for (int hw : plans[t].merges)
       DA_TRY(ck(r->gq_recv[2 * hw + static_cast<int>(t % 2)].ensure(g_q), "da_rank workspace"));
+  // split step (balanced_split backward): kv row halves lo = [0, c/2), hi = [c/2, c)
+  const int64_t lo = rows / 2, hi = rows - lo;
+  bool split = false;
+  for (const Plan& p : plans)
+    split = split || p.part != kPartWhole || !p.kvh_sends.empty() || p.gradkv_part != kPartWhole;
+  const size_t half_b = static_cast<size_t>(h_kv) * hi * 256;      // bf16 k or v half
+  const size_t gh_b = static_cast<size_t>(h_kv) * hi * 128 * 4;    // fp32 dk or dv half
+  const size_t glo_b = static_cast<size_t>(h_kv) * (lo > 0 ? lo : 1) * 128 * 4;
+  if (split) {
+    DA_TRY(ck(r->k_lo.ensure(static_cast<size_t>(h_kv) * (lo > 0 ? lo : 1) * 256),
+              "da_rank workspace"));
+    DA_TRY(ck(r->v_lo.ensure(static_cast<size_t>(h_kv) * (lo > 0 ? lo : 1) * 256),
+              "da_rank workspace"));
+    DA_TRY(ck(r->k_hi.ensure(half_b), "da_rank workspace"));
+    DA_TRY(ck(r->v_hi.ensure(half_b), "da_rank workspace"));
+    DA_TRY(ck(r->kvh.ensure(2 * half_b), "da_rank workspace"));
+    DA_TRY(ck(r->gh_send.ensure(2 * gh_b), "da_rank workspace"));
+    DA_TRY(ck(r->gh_recv.ensure(2 * gh_b), "da_rank workspace"));
+    DA_TRY(ck(r->dkv_lo.ensure(2 * glo_b), "da_rank workspace"));
+    cudaError_t e = cudaSuccess;  // this pass's k / v (a restored layer may differ)
+    if (lo > 0) e = pack_rows(r->k, r->k_lo.p, h_kv, rows, 0, lo, st);
+    if (e == cudaSuccess && lo > 0) e = pack_rows(r->v, r->v_lo.p, h_kv, rows, 0, lo, st);
+    if (e == cudaSuccess) e = pack_rows(r->k, r->k_hi.p, h_kv, rows, lo, hi, st);
+    if (e == cudaSuccess) e = pack_rows(r->v, r->v_hi.p, h_kv, rows, lo, hi, st);
+    DA_TRY(ck(e, "da_rank_backward split pack"));
+  }
   DA_TRY(ck(cudaMemsetAsync(dq, 0, g_q, st), "dq zero"));
   DA_TRY(ck(cudaMemsetAsync(dk, 0, g_kv, st), "dk zero"));
   DA_TRY(ck(cudaMemsetAsync(dv, 0, g_kv, st), "dv zero"));
@@ -947,6 +1013,14 @@ static da_status rank_backward_flat(da_rank* r, const FlatSchedule& sch, const v
   r->key_bytes[kLse] = r->key_bytes[kDVec] = static_cast<size_t>(nq) * 4;
   for (Key key : {kGK0, kGV0, kGK1, kGV1}) r->key_bytes[key] = g_kv;
   r->key_bytes[kGQ0] = r->key_bytes[kGQ1] = g_q;
+  if (split) {
+    r->local[kKHi] = r->k_hi.p;
+    r->local[kVHi] = r->v_hi.p;
+    r->local[kGKH] = r->gh_send.p;
+    r->local[kGVH] = r->gh_send.as<char>() + gh_b;
+    r->key_bytes[kKHi] = r->key_bytes[kVHi] = half_b;
+    r->key_bytes[kGKH] = r->key_bytes[kGVH] = gh_b;
+  }
   if (P > 1) DA_TRY(begin_pass(r));
 
   da_counters c{};
@@ -960,7 +1034,12 @@ static da_status rank_backward_flat(da_rank* r, const FlatSchedule& sch, const v
     DA_TRY(wait_work(r, &res_w[tt % 2], st));
     cudaEvent_t fe0 =
         (!pp.gradkv_from.empty() || !pp.merges.empty()) ? trace_event(r, st) : nullptr;
-    if (!pp.gradkv_from.empty()) {
+    if (!pp.gradkv_from.empty() && pp.gradkv_part == kPartHigh) {  // rows [lo, rows)
+      count(c, kMsgGradKV, 2 * h_kv * hi * 128);
+      const float* g = r->gh_recv.as<float>();
+      DA_TRY(ck(launch_add_rows(dk, g, h_kv, rows, lo, hi, st), "GradKV fold"));
+      DA_TRY(ck(launch_add_rows(dv, g + h_kv * hi * 128, h_kv, rows, lo, hi, st), "GradKV fold"));
+    } else if (!pp.gradkv_from.empty()) {
       count(c, kMsgGradKV, 2 * nkv * 128);
       const float* g = r->g_recv[tt % 2].as<float>();
       DA_TRY(ck(launch_add(dk, g, nkv * 128, st), "GradKV fold"));
@@ -988,15 +1067,39 @@ static da_status rank_backward_flat(da_rank* r, const FlatSchedule& sch, const v
     cudaEvent_t te0 = p.action ? trace_event(r, st) : nullptr;
     if (p.action == 1) {
       ++c.attention_kernel_calls;
-      DA_TRY(bwd_chunk(r->q, r->k, r->v, d_out, r->lse, r->d_vec.as<float>(), h_q, h_kv, rows, dq,
-                       dk, dv, true, DA_MASK_DIAGONAL, det, st));
+      DA_TRY(bwd_chunk(r->q, r->k, r->v, d_out, r->lse, r->d_vec.as<float>(), h_q, h_kv, rows,
+                       rows, dq, dk, dv, true, DA_MASK_DIAGONAL, det, st));
+    } else if (p.action == 2 && p.part == kPartHigh) {  // split step: high half of the kv rows
+      ++c.attention_kernel_calls;
+      count(c, kMsgKV, 2 * h_kv * hi * 128);
+      const char* ks = r->kvh.as<char>();
+      float* gk = r->gh_send.as<float>();
+      DA_TRY(bwd_chunk(r->q, ks, ks + half_b, d_out, r->lse, r->d_vec.as<float>(), h_q, h_kv,
+                       rows, hi, dq, gk, gk + h_kv * hi * 128, false, DA_MASK_FULL, det, st));
+    } else if (p.action == 3 && p.part == kPartLow) {  // split step: low half of my kv rows
+      ++c.attention_kernel_calls;
+      c.q_scalars += rows * (2 * 128 + 2) * h_q;
+      ++c.q_messages;
+      const char* b = r->bundle[t % 2].as<char>();
+      float* gq = r->q_send[t % 2].as<float>();
+      float* gl = r->dkv_lo.as<float>();
+      DA_TRY(ck(cudaMemsetAsync(gq, 0, g_q, st), "gq zero"));
+      if (lo > 0) {
+        DA_TRY(bwd_chunk(b, r->k_lo.p, r->v_lo.p, b + q_b,
+                         reinterpret_cast<const float*>(b + 2 * q_b),
+                         reinterpret_cast<const float*>(b + 2 * q_b + nq * 4), h_q, h_kv, rows, lo,
+                         gq, gl, gl + h_kv * lo * 128, false, DA_MASK_FULL, det, st));
+        DA_TRY(ck(launch_add_rows(dk, gl, h_kv, rows, 0, lo, st), "low-half fold"));
+        DA_TRY(ck(launch_add_rows(dv, gl + h_kv * lo * 128, h_kv, rows, 0, lo, st),
+                  "low-half fold"));
+      }
     } else if (p.action == 2) {
       ++c.attention_kernel_calls;
       count(c, kMsgKV, 2 * nkv * 128);
       const char* ks = r->kv_slot[t % 2].as<char>();
       float* gk = r->g_send[t % 2].as<float>();
       DA_TRY(bwd_chunk(r->q, ks, ks + kv_b, d_out, r->lse, r->d_vec.as<float>(), h_q, h_kv, rows,
-                       dq, gk, gk + nkv * 128, false, DA_MASK_FULL, det, st));
+                       rows, dq, gk, gk + nkv * 128, false, DA_MASK_FULL, det, st));
     } else if (p.action == 3) {
       ++c.attention_kernel_calls;
       c.q_scalars += rows * (2 * 128 + 2) * h_q;
@@ -1005,8 +1108,8 @@ static da_status rank_backward_flat(da_rank* r, const FlatSchedule& sch, const v
       float* gq = r->q_send[t % 2].as<float>();
       DA_TRY(ck(cudaMemsetAsync(gq, 0, g_q, st), "gq zero"));
       DA_TRY(bwd_chunk(b, r->k, r->v, b + q_b, reinterpret_cast<const float*>(b + 2 * q_b),
-                       reinterpret_cast<const float*>(b + 2 * q_b + nq * 4), h_q, h_kv, rows, gq,
-                       dk, dv, true, DA_MASK_FULL, det, st));
+                       reinterpret_cast<const float*>(b + 2 * q_b + nq * 4), h_q, h_kv, rows, rows,
+                       gq, dk, dv, true, DA_MASK_FULL, det, st));
     }
     if (p.action) trace_push(r, 0, p.action, t, p.action == 1 ? w : p.peer, -1, te0,
                              trace_event(r, st));

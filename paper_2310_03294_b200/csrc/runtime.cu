@@ -34,6 +34,8 @@ struct Workspace {
   std::vector<float*> dvec;       // per worker D (backward)
   void* kv_half = nullptr;        // packed k, v row half (split schedule), bf16
   size_t kv_half_bytes = 0;
+  void* dkv_half = nullptr;       // dk, dv of a kv row half (split backward), fp32
+  size_t dkv_half_bytes = 0;
   int* flag = nullptr;
   std::vector<void*> allocs;
   cudaStream_t stream = nullptr;
@@ -45,7 +47,26 @@ struct Workspace {
     flag = nullptr;
     kv_half = nullptr;
     kv_half_bytes = 0;
+    dkv_half = nullptr;
+    dkv_half_bytes = 0;
     P = 0;
+  }
+
+  // grows one of the split-schedule buffers (kv_half / dkv_half) to `bytes`
+  cudaError_t grow(void** buf, size_t* cap, size_t bytes) {
+    if (*cap >= bytes) return cudaSuccess;
+    if (*buf) {
+      cudaFree(*buf);
+      for (auto& a : allocs)
+        if (a == *buf) a = nullptr;
+      *buf = nullptr;
+      *cap = 0;
+    }
+    cudaError_t e = cudaMalloc(buf, bytes);
+    if (e != cudaSuccess) return e;
+    allocs.push_back(*buf);
+    *cap = bytes;
+    return cudaSuccess;
   }
   ~Workspace() { release(); }
 
@@ -241,17 +262,8 @@ static da_status run_forward_flat(const da_shards* s, const FlatSchedule& sch,
         const int64_t r0 = k.helper == kPartLow ? 0 : lo;
         const int64_t n = k.helper == kPartLow ? lo : s->rows - lo;
         const size_t bytes = static_cast<size_t>(s->h_kv) * (s->rows - lo) * s->d * 2 * 2;
-        if (g_ws.kv_half_bytes < bytes) {
-          if (g_ws.kv_half) {
-            cudaFree(g_ws.kv_half);
-            for (auto& a : g_ws.allocs)
-              if (a == g_ws.kv_half) a = nullptr;
-          }
-          e = cudaMalloc(&g_ws.kv_half, bytes);
-          if (e != cudaSuccess) return cuda_error(e, "run_forward split workspace");
-          g_ws.allocs.push_back(g_ws.kv_half);
-          g_ws.kv_half_bytes = bytes;
-        }
+        e = g_ws.grow(&g_ws.kv_half, &g_ws.kv_half_bytes, bytes);
+        if (e != cudaSuccess) return cuda_error(e, "run_forward split workspace");
         void* kh = g_ws.kv_half;
         void* vh = static_cast<char*>(g_ws.kv_half) + bytes / 2;
         e = pack_rows(s->k[k.kv_owner - 1], kh, s->h_kv, s->rows, r0, n, s->d, st);
@@ -333,7 +345,9 @@ da_status da_run_backward(const da_shards* s, da_counters* counters, void* strea
 // Backward over a ring or balanced backward schedule. Every pair (q chunk p,
 // kv chunk r) is one block_attn_backward launch; dq goes to p's accumulator,
 // dk/dv to r's (zero-copy GradKV / local for helpers). Ring order reproduces
-// runtime.cpp:605-651; balanced order follows make_balanced_backward.
+// runtime.cpp:605-651; balanced order follows make_balanced_backward. A split
+// step's halves (make_balanced_split_backward) pack the kv rows, compute into
+// a half-size dk/dv and fold it into the kv owner's rows.
 static da_status run_backward_flat(const da_shards* s, const FlatSchedule& sch,
                                    da_counters* counters, void* stream) {
   da_status rc = check_shards(s, true);
@@ -360,6 +374,48 @@ static da_status run_backward_flat(const da_shards* s, const FlatSchedule& sch,
     if (e != cudaSuccess) return cuda_error(e, "run_backward setup");
   }
   std::vector<Tally> tally(P);
+  // one pair (q chunk qw, kv chunk kvw) on kv rows [r0, r0 + n) (part of the
+  // split step: packed k/v half in, that half's dk/dv folded into kvw's rows)
+  const int64_t lo = s->rows / 2;
+  auto chunk_part = [&](int qw, int kvw, int part) -> da_status {
+    const int64_t r0 = part == kPartHigh ? lo : 0;
+    const int64_t n = part == kPartLow ? lo : s->rows - lo;
+    const size_t kv_b = static_cast<size_t>(s->h_kv) * (s->rows - lo) * s->d * 2;
+    const size_t g_b = static_cast<size_t>(s->h_kv) * (s->rows - lo) * s->d * 4;
+    cudaError_t e2 = g_ws.grow(&g_ws.kv_half, &g_ws.kv_half_bytes, 2 * kv_b);
+    if (e2 == cudaSuccess) e2 = g_ws.grow(&g_ws.dkv_half, &g_ws.dkv_half_bytes, 2 * g_b);
+    if (e2 != cudaSuccess) return cuda_error(e2, "run_backward split workspace");
+    void* kh = g_ws.kv_half;
+    void* vh = static_cast<char*>(g_ws.kv_half) + kv_b;
+    float* gk = static_cast<float*>(g_ws.dkv_half);
+    float* gv = reinterpret_cast<float*>(static_cast<char*>(g_ws.dkv_half) + g_b);
+    e2 = pack_rows(s->k[kvw - 1], kh, s->h_kv, s->rows, r0, n, s->d, st);
+    if (e2 == cudaSuccess) e2 = pack_rows(s->v[kvw - 1], vh, s->h_kv, s->rows, r0, n, s->d, st);
+    if (e2 != cudaSuccess) return cuda_error(e2, "run_backward split pack");
+    da_bwd_args a{};
+    a.q = s->q[qw - 1];
+    a.k = kh;
+    a.v = vh;
+    a.d_out = s->d_out[qw - 1];
+    a.lse = s->lse[qw - 1];
+    a.d_vec = g_ws.dvec[qw - 1];
+    a.h_q = s->h_q;
+    a.h_kv = s->h_kv;
+    a.rows_q = s->rows;
+    a.rows_kv = n;
+    a.d = s->d;
+    a.dq_acc = s->dq[qw - 1];
+    a.dk_acc = gk;
+    a.dv_acc = gv;
+    a.accumulate_kv = 0;
+    a.scale = 0.f;
+    a.mask = DA_MASK_FULL;
+    da_status r2 = da_attn_bwd_chunk(&a, st);
+    if (r2 != DA_OK) return r2;
+    e2 = launch_add_rows(s->dk[kvw - 1], gk, s->h_kv, s->rows, r0, n, st);
+    if (e2 == cudaSuccess) e2 = launch_add_rows(s->dv[kvw - 1], gv, s->h_kv, s->rows, r0, n, st);
+    return e2 == cudaSuccess ? DA_OK : cuda_error(e2, "run_backward split fold");
+  };
   auto chunk = [&](int qw, int kvw, int mask) {
     da_bwd_args a{};
     a.q = s->q[qw - 1];
@@ -388,18 +444,22 @@ static da_status run_backward_flat(const da_shards* s, const FlatSchedule& sch,
       const int w = k.worker;
       Tally& me = tally[w - 1];
       ++me.c.attention_kernel_calls;
+      const int part = k.kind == kRemote ? k.helper : kPartWhole;
       if (k.kind == kLocal) {
         rc = chunk(w, w, DA_MASK_DIAGONAL);
-      } else if (k.worker == k.query_owner) {  // direct: KV in, GradKV out
-        count(me.c, kMsgKV, R, D, s->h_kv);
+      } else if (k.worker == k.query_owner) {  // direct: KV (half) in, GradKV out
+        count(me.c, part == kPartWhole ? kMsgKV : kMsgKVHalf,
+              part == kPartWhole ? R : R - lo, D, s->h_kv);
         me.acquire();
-        rc = chunk(w, k.kv_owner, DA_MASK_FULL);
+        rc = part == kPartWhole ? chunk(w, k.kv_owner, DA_MASK_FULL)
+                                : chunk_part(w, k.kv_owner, part);
         me.release();
       } else {  // helper: (q, dO, lse, D) bundle in, dq partial out
         me.acquire();
         me.c.q_scalars += R * (2 * D + 2) * s->h_q;
         ++me.c.q_messages;
-        rc = chunk(k.query_owner, w, DA_MASK_FULL);
+        rc = part == kPartWhole ? chunk(k.query_owner, w, DA_MASK_FULL)
+                                : chunk_part(k.query_owner, w, part);
         me.release();
       }
       if (rc != DA_OK) return rc;
@@ -411,7 +471,12 @@ static da_status run_backward_flat(const da_shards* s, const FlatSchedule& sch,
       if (m.step != t) continue;
       if (m.kind == kMsgGradKV) {
         Tally& me = tally[m.to - 1];
-        count(me.c, kMsgGradKV, R, D, s->h_kv);
+        int part = kPartWhole;  // the sender's direct task of this step: a half's GradKV
+        for (const Task& k : sch.tasks)
+          if (k.step == t && k.kind == kRemote && k.worker == m.from && k.query_owner == m.from)
+            part = k.helper;
+        count(me.c, kMsgGradKV, part == kPartWhole ? R : (part == kPartLow ? lo : R - lo), D,
+              s->h_kv);
         me.acquire();
         me.release();
       } else if (m.kind == kMsgPartial) {
@@ -468,6 +533,8 @@ da_status da_run_backward_sched(const da_shards* s, int schedule_kind, da_counte
     return run_backward_flat(s, make_ring_backward(P), counters, stream);
   if (schedule_kind == DA_SCHEDULE_BALANCED_BWD || schedule_kind == DA_SCHEDULE_BALANCED)
     return run_backward_flat(s, make_balanced_backward(P), counters, stream);
+  if (schedule_kind == DA_SCHEDULE_BALANCED_SPLIT_BWD || schedule_kind == DA_SCHEDULE_BALANCED_SPLIT)
+    return run_backward_flat(s, make_balanced_split_backward(P), counters, stream);
   return set_error(DA_ERR_CONFIG, "unknown schedule kind");
 }
 

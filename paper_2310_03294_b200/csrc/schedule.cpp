@@ -244,6 +244,9 @@ static FlatSchedule with_grad_kv(FlatSchedule s) {
 
 FlatSchedule make_ring_backward(int P) { return with_grad_kv(make_ring(P)); }
 FlatSchedule make_balanced_backward(int P) { return with_grad_kv(make_balanced(P)); }
+FlatSchedule make_balanced_split_backward(int P) {
+  return with_grad_kv(make_balanced_split(P));
+}
 
 std::vector<std::string> validate_backward_flat(const FlatSchedule& s) {
   FlatSchedule fwd = s;
@@ -292,6 +295,7 @@ da_status da_schedule_build(int workers, int kind, int32_t* steps_out, int32_t* 
     case DA_SCHEDULE_RING_BWD: s = da::make_ring_backward(workers); break;
     case DA_SCHEDULE_BALANCED_BWD: s = da::make_balanced_backward(workers); break;
     case DA_SCHEDULE_BALANCED_SPLIT: s = da::make_balanced_split(workers); break;
+    case DA_SCHEDULE_BALANCED_SPLIT_BWD: s = da::make_balanced_split_backward(workers); break;
     default: return da::set_error(DA_ERR_CONFIG, "unknown schedule kind");
   }
   if (steps_out) *steps_out = s.steps;

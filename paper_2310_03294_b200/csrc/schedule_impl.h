@@ -54,6 +54,10 @@ std::vector<std::string> validate_flat(const FlatSchedule& s);
 // Ring backward = the reference run_backward order (runtime.cpp:605-651).
 FlatSchedule make_ring_backward(int P);
 FlatSchedule make_balanced_backward(int P);
+// make_balanced_split's table with the backward messages (GradKV of the high
+// half for the split direct pairs): no worker idles at t = P/2 in the backward
+// either. Identical to make_balanced_backward for odd P.
+FlatSchedule make_balanced_split_backward(int P);
 // validate_flat's invariants plus: every direct pair (p, r) returns a GradKV
 // p -> r no earlier than its step, and no other GradKV exists.
 std::vector<std::string> validate_backward_flat(const FlatSchedule& s);

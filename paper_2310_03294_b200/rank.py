@@ -18,7 +18,7 @@ from .runtime import CommCounters
 
 _AG = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p)
 _FWD = {"ring": 0, "balanced": 1, "balanced_split": 4}
-_BWD = {"ring": 2, "balanced": 3}
+_BWD = {"ring": 2, "balanced": 3, "balanced_split": 5}
 
 
 class RankRuntime:
@@ -199,8 +199,9 @@ def _counters(c) -> CommCounters:
 
 # buffer keys of csrc/rank_runtime.cu -> the reference's PayloadKind names
 _FWD_KIND = {0: "kv", 1: "kv", 2: "q", 3: "partial", 4: "kv_half", 5: "kv_half"}
-_BWD_KIND = {0: "kv", 1: "kv", 2: "q", 6: "q", 7: "q", 8: "q", 9: "grad_kv", 10: "grad_kv",
-             11: "grad_kv", 12: "grad_kv", 13: "partial", 14: "partial"}
+_BWD_KIND = {0: "kv", 1: "kv", 2: "q", 4: "kv_half", 5: "kv_half", 6: "q", 7: "q", 8: "q",
+             9: "grad_kv", 10: "grad_kv", 11: "grad_kv", 12: "grad_kv", 13: "partial",
+             14: "partial", 15: "grad_kv", 16: "grad_kv"}
 _TASK = {1: "local_attn", 2: "remote_attn", 3: "helper_attn", 4: "rescale_merge", 5: "fold"}
 
 

@@ -214,7 +214,8 @@ def run_backward(shards: list[SequenceShard], schedule="ring",
                  stream=None) -> ExecutionTrace:
     """runtime.cpp:720-750. schedule="ring" is the reference order
     (BackwardMode::Vanilla); "balanced" is the load-balanced backward
-    extension (schedule.build_balanced_backward_schedule). Requires forward
+    extension (schedule.build_balanced_backward_schedule), "balanced_split"
+    its even-P split (build_balanced_split_backward_schedule). Requires forward
     state and d_out; writes fp32 dq/dk/dv into the shards."""
     for s in shards:
         if not s.has_forward_state():
@@ -234,10 +235,10 @@ def run_backward(shards: list[SequenceShard], schedule="ring",
     strm = stream if stream is not None else torch.cuda.current_stream()
     sptr = C.c_void_p(strm.cuda_stream)
     if isinstance(schedule, str):
-        if schedule not in ("ring", "balanced"):
+        if schedule not in ("ring", "balanced", "balanced_split"):
             from .errors import ConfigError
             raise ConfigError(f"unknown backward schedule {schedule!r}")
-        kind = {"ring": 2, "balanced": 3}[schedule]
+        kind = {"ring": 2, "balanced": 3, "balanced_split": 5}[schedule]
         check(_lib.lib().da_run_backward_sched(C.byref(st), kind, C.byref(c), sptr))
     else:  # a backward schedule table (validate_backward invariants)
         steps, t, nt, m, nm = _table(schedule)

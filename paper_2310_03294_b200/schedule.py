@@ -157,6 +157,15 @@ def build_balanced_backward_schedule(workers: int) -> Schedule:
     return _build(workers, 3)
 
 
+def build_balanced_split_backward_schedule(workers: int) -> Schedule:
+    """Backward of the split schedule (extension; DA_SCHEDULE_BALANCED_SPLIT_BWD):
+    the balanced_split task table with the backward messages. At t = P/2 the
+    owner computes its pair on the high half of the kv rows (KVHalf in, that
+    half's GradKV back) and the helper on the low half (Q bundle in, dq
+    Partial back). Odd P: the balanced backward."""
+    return _build(workers, 5)
+
+
 def validate_backward(s: Schedule) -> list:
     """validate() plus GradKV coverage of every direct pair."""
     return validate(s, backward=True)

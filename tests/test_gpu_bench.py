@@ -28,7 +28,7 @@ def test_bench_two_ranks_self_spawned(cuda):
     assert j["n_gpus"] == 2 and j["steps"] == 2 and j["warmup"] == 3
     assert j["metric"] == "attn fwd+bwd TFLOP/s" and j["value"] > 0 and j["scaling"] == "strong"
     assert j["config"]["transport"] == "ipc" and j["config"]["seq_len"] == 4096
-    assert {"balanced_split+balanced", "ring+ring", "balanced+balanced", "nocomm"} <= set(j["legs"])
+    assert {"balanced_split+balanced_split", "ring+ring", "balanced+balanced", "nocomm"} <= set(j["legs"])
     assert j["balanced_speedup_vs_ring"] > 0 and j["exposed_comm_pct"] is not None
     roof = j["roofline"]
     assert roof["bound"] in ("tensor", "nvlink") and roof["nvlink_bytes_per_gpu"] > 0
@@ -58,7 +58,7 @@ def test_bench_eight_ranks_self_spawned(cuda):
     assert r.returncode == 0, r.stderr[-4000:]
     j = _line(r.stdout)
     assert j["n_gpus"] == 8 and j["config"]["tokens_per_gpu"] == 1024
-    assert {"balanced_split+balanced", "ring+ring", "balanced+balanced", "nocomm"} <= set(j["legs"])
+    assert {"balanced_split+balanced_split", "ring+ring", "balanced+balanced", "nocomm"} <= set(j["legs"])
 
 
 def test_bench_nccl_failure_falls_back_to_ipc(cuda):

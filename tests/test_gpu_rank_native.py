@@ -68,11 +68,15 @@ def _rel(a, b):
     (3, 768, 2, "ring", "balanced", None), (4, 1024, 2, "balanced_split", "ring", None),
     (1, 512, 2, "balanced", "ring", None), (2, 1002, 1, "balanced_split", "balanced", None),
     (4, 1024, 4, "balanced", "balanced", 2), (8, 2048, 2, "balanced_split", "balanced", None),
-    (8, 2048, 4, "balanced", "ring", 1)])
+    (8, 2048, 4, "balanced", "ring", 1), (2, 1002, 1, "balanced_split", "balanced_split", None),
+    (4, 1024, 2, "balanced_split", "balanced_split", None),
+    (4, 1024, 4, "balanced_split", "balanced_split", 2),
+    (8, 2048, 2, "balanced_split", "balanced_split", None),
+    (3, 768, 2, "balanced", "balanced_split", None)])
 def test_native_rank_runtime(cuda, world, n, heads, fwd, bwd, heads_kv):
     """Worlds 1-4 and 8 (the SCALE run's P), ring / balanced / split forward,
-    ring / balanced backward, odd chunk rows (split halves 250 / 251), GQA
-    (4 q / 2 kv and 4 q / 1 kv heads)."""
+    ring / balanced / split backward, odd chunk rows (split halves 250 / 251),
+    GQA (4 q / 2 kv and 4 q / 1 kv heads)."""
     with tempfile.TemporaryDirectory() as td:
         mp.spawn(_worker, args=(world, _port(), n, heads, fwd, bwd, td, heads_kv), nprocs=world,
                  join=True)
@@ -112,7 +116,8 @@ def test_native_rank_runtime(cuda, world, n, heads, fwd, bwd, heads_kv):
     assert np.array_equal(got["lse"], torch.cat([s.lse for s in shards], 1).cpu().numpy())
 
 
-@pytest.mark.parametrize("world,fwd,bwd", [(3, "balanced", "balanced"), (4, "balanced_split", "ring")])
+@pytest.mark.parametrize("world,fwd,bwd", [(3, "balanced", "balanced"), (4, "balanced_split", "ring"),
+                                           (4, "balanced_split", "balanced_split")])
 def test_native_rank_runtime_deterministic_backward(cuda, world, fwd, bwd):
     """deterministic=True: the distributed backward repeats bit for bit (the
     reference's executors do, runtime.hpp:7-9) and still matches the oracle."""
@@ -189,7 +194,8 @@ def _trace_worker(rank, world, port, outdir, fwd, bwd):
         tdist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,fwd,bwd", [(4, "balanced", "ring"), (4, "balanced_split", "balanced")])
+@pytest.mark.parametrize("world,fwd,bwd", [(4, "balanced", "ring"), (4, "balanced_split", "balanced"),
+                                           (4, "balanced_split", "balanced_split")])
 def test_native_runtime_wall_clock_trace(cuda, world, fwd, bwd):
     """SURVEY §8(f)4 on the product path: the native runtime's CUDA-event trace
     in the reference's ExecutionTrace schema (runtime.cpp:752-782): one event
@@ -224,8 +230,9 @@ def test_native_runtime_wall_clock_trace(cuda, world, fwd, bwd):
     merges = sum(1 for st in sched.steps for x in st if x.kind == S.TaskKind.RescaleMerge)
     assert sum(1 for w in tf["workers"] for e in w["events"]
                if e["task"].startswith("rescale_merge")) == merges
-    bsched = (S.build_ring_backward_schedule if bwd == "ring" else
-              S.build_balanced_backward_schedule)(world)
+    bsched = {"ring": S.build_ring_backward_schedule,
+              "balanced": S.build_balanced_backward_schedule,
+              "balanced_split": S.build_balanced_split_backward_schedule}[bwd](world)
     assert sorted((m["kind"], m["from"], m["to"]) for m in tb["messages"]) == \
         sorted((kinds[int(m.kind)], m.from_, m.to) for m in bsched.messages)
     assert tf["counters"]["kv_messages"] == sum(1 for m in sched.messages if int(m.kind) in (0, 4))

@@ -164,6 +164,22 @@ def test_balanced_split_forward(cuda, P, n, heads, heads_kv):
     _check_against_oracle(shards, P, n, "balanced_split", heads, tf, tb, heads_kv=heads_kv)
 
 
+@pytest.mark.parametrize("P,n,heads,heads_kv", [(4, 4096, 1, 1), (2, 1002, 1, 1), (8, 2048, 2, 2),
+                                                (4, 1024, 4, 2), (5, 1280, 1, 1)])
+def test_balanced_split_backward(cuda, P, n, heads, heads_kv):
+    """Backward of the split schedule (extension): the split step's halves on
+    packed kv rows, their dk/dv folded into the kv owner's rows; gradients and
+    counters (H=1) equal to the oracle running the same table; odd P is the
+    balanced backward."""
+    from paper_2310_03294_b200.runtime import make_parity_shards, run_backward, run_forward
+    shards = make_parity_shards(6, P, n, heads, 128, heads_kv=heads_kv)
+    tf = run_forward(shards, "balanced_split")
+    tb = run_backward(shards, "balanced_split")
+    torch.cuda.synchronize()
+    _check_against_oracle(shards, P, n, "balanced_split", heads, tf, tb, heads_kv=heads_kv,
+                          bwd="balanced_split")
+
+
 def test_p1_backward_is_the_single_chunk_kernel(cuda):
     """test_runtime.cpp:201-213: with one worker the runtime backward is one
     block_attn_backward call (dk/dv bitwise; dq to fp32 reduction order)."""

@@ -18,9 +18,9 @@ from paper_2310_03294_b200 import _lib
 from paper_2310_03294_b200.errors import check
 
 FWD = {"ring": 0, "balanced": 1, "balanced_split": 4}
-BWD = {"ring": 2, "balanced": 3}
+BWD = {"ring": 2, "balanced": 3, "balanced_split": 5}
 KEYS = ["k", "v", "q", "part", "k_hi", "v_hi", "d_out", "lse", "d_vec", "gk0", "gv0", "gk1",
-        "gv1", "gq0", "gq1"]
+        "gv1", "gq0", "gq1", "gk_half", "gv_half"]
 
 
 def protocol(world, rank, fwd, bwd):
@@ -33,7 +33,8 @@ def protocol(world, rank, fwd, bwd):
 
 
 @pytest.mark.parametrize("fwd,bwd", [("ring", "ring"), ("balanced", "balanced"),
-                                     ("balanced_split", "ring"), ("balanced_split", "balanced")])
+                                     ("balanced_split", "ring"), ("balanced_split", "balanced"),
+                                     ("balanced_split", "balanced_split")])
 @pytest.mark.parametrize("world", list(range(1, 17)))
 def test_every_send_meets_its_receive_in_the_same_phase(world, fwd, bwd):
     sends = defaultdict(list)  # (pass, phase, src, dst) -> keys in issue order

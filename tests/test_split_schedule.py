@@ -115,3 +115,50 @@ def test_oracle_stepper_split_matches_dense_and_balanced(P, n):
     assert c_s[1] == c_b[1] + (P // 2) * rows * 16
     assert c_s[2] == c_b[2] + (P // 2) * rows * 18
     assert c_s[8] == c_b[8] + P // 2  # attention kernel calls
+
+
+def test_split_backward_table():
+    """Backward of the split schedule (DA_SCHEDULE_BALANCED_SPLIT_BWD): the split
+    task table plus one GradKV per direct task (the half's for the split step),
+    valid under the backward invariants, no idle slot; odd P = balanced backward."""
+    for P in range(1, 33):
+        s = S.build_balanced_split_backward_schedule(P)
+        assert S.validate_backward(s) == [], P
+        assert s.steps == S.build_balanced_split_schedule(P).steps
+        assert s.idle_slot_count() == 0
+        grads = sorted((m.step, m.from_, m.to) for m in s.messages
+                       if m.kind == S.PayloadKind.GradKV)
+        direct = sorted((t_, t.worker, t.kv_owner) for t_, st in enumerate(s.steps) for t in st
+                        if t.kind == K.RemoteAttn and t.worker == t.query_owner)
+        assert grads == direct
+        if P % 2:
+            assert s.flat() == S.build_balanced_backward_schedule(P).flat()
+    # P = 4, t = 2: owners 3 / 4 take the high halves of kv 1 / 2 (KVHalf in, GradKV
+    # of the half back); helpers 1 / 2 the low halves (Q bundle in, dq Partial back)
+    s4 = S.build_balanced_split_backward_schedule(4)
+    last = sorted((m.from_, m.to, m.kind.name) for m in s4.messages if m.step == 2)
+    assert last == [(1, 3, "KVHalf"), (1, 3, "PartialResult"), (2, 4, "KVHalf"),
+                    (2, 4, "PartialResult"), (3, 1, "GradKV"), (3, 1, "Q"), (4, 2, "GradKV"),
+                    (4, 2, "Q")]
+
+
+@pytest.mark.parametrize("P,n", [(2, 64), (4, 128), (6, 96), (8, 256), (4, 132), (3, 96)])
+def test_oracle_split_backward_matches_ring(P, n):
+    """The oracle's backward over the split table gives the reference ring
+    backward's gradients (fp64, to summation order); counters: the split step
+    moves half a KV chunk and half a GradKV per owner, plus a Q bundle and a dq
+    Partial per helper."""
+    q, k, v, do = O.make_inputs(4, P, n, 16, 1)
+    q, k, v, do = q[0], k[0], v[0], do[0]
+    out, lse, _ = O.run_forward(q, k, v, P, "balanced")
+    dq_r, dk_r, dv_r, _ = O.run_backward(q, k, v, out, lse, do, P)
+    dq_s, dk_s, dv_s, c_s = O.run_backward_sched(q, k, v, out, lse, do, P, "balanced_split")
+    _, _, _, c_b = O.run_backward_sched(q, k, v, out, lse, do, P, "balanced")
+    for a, b in ((dq_s, dq_r), (dk_s, dk_r), (dv_s, dv_r)):
+        assert np.abs(a - b).max() < 1e-12
+    rows, half = n // P, (P // 2 if P % 2 == 0 else 0)
+    hi = rows - rows // 2
+    assert c_s[0] == c_b[0] - half * 2 * rows * 16 + half * 2 * hi * 16   # KV / KVHalf
+    assert c_s[3] == c_b[3] - half * 2 * rows * 16 + half * 2 * hi * 16   # GradKV halves
+    assert c_s[1] == c_b[1] + half * rows * (2 * 16 + 2)                  # Q bundles
+    assert c_s[8] == c_b[8] + half                                         # kernel calls

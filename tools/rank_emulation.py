@@ -28,7 +28,8 @@ from paper_2310_03294_b200.rank import RankRuntime  # noqa: E402
 
 D = 128
 LEGS = (("ring+ring", "ring", "ring"), ("balanced+balanced", "balanced", "balanced"),
-        ("balanced_split+balanced", "balanced_split", "balanced"))
+        ("balanced_split+balanced", "balanced_split", "balanced"),
+        ("balanced_split+balanced_split", "balanced_split", "balanced_split"))
 
 
 def rank_time(r, world, rows, heads, hkv, fwd, bwd, steps, warmup):
