@@ -57,7 +57,8 @@ def _worker(rank, world, port, outdir, h, hkv, fwd, bwd):
 
 
 @pytest.mark.parametrize("world,h,hkv,fwd,bwd", [(2, 2, 2, "balanced", "ring"),
-                                                 (4, 4, 1, "balanced_split", "balanced")])
+                                                 (4, 4, 1, "balanced_split", "balanced"),
+                                                 (4, 2, 2, "balanced_split", "balanced_split")])
 def test_runtime_32k_every_element_vs_fp32(cuda, world, h, hkv, fwd, bwd):
     with tempfile.TemporaryDirectory() as td:
         mp.spawn(_worker, args=(world, _port(), td, h, hkv, fwd, bwd), nprocs=world, join=True)

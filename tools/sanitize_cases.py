@@ -1,7 +1,9 @@
 """Small launches of every kernel for compute-sanitizer (tools/sanitize.sh):
 forward (diagonal / full / ragged / chained accumulator / empty), merge,
 finalize, backward preprocess, backward (diagonal / full ragged / GQA /
-deterministic), bf16 conversion."""
+deterministic), bf16 conversion, the P-worker executor (incl. the split
+backward), the host pipeline and the host-buffer entry points. With
+DA_FWD_KERNEL=pair every forward runs on the CTA-pair kernel."""
 import sys
 from pathlib import Path
 
@@ -41,7 +43,8 @@ def main():
                           accumulate_kv=True)
     # the native P-worker executor (schedules, message buffers, merges, split halves)
     from paper_2310_03294_b200.runtime import make_parity_shards, run_backward, run_forward
-    for kind, bwd in (("balanced", "ring"), ("balanced_split", "balanced"), ("ring", "ring")):
+    for kind, bwd in (("balanced", "ring"), ("balanced_split", "balanced"), ("ring", "ring"),
+                      ("balanced_split", "balanced_split")):
         shards = make_parity_shards(3, 4, 1024, 2, 128, heads_kv=1)
         run_forward(shards, kind)
         run_backward(shards, bwd)
