@@ -28,6 +28,14 @@
 #include "capi_internal.h"
 #include "kernels.h"
 
+// cost probe only (variant builds): the same pipeline with every host<->device
+// copy skipped, which separates the copies' cost from the grouping's
+#ifdef DA_PIPELINE_PROBE_NO_COPIES
+constexpr bool kCopies = false;
+#else
+constexpr bool kCopies = true;
+#endif
+
 struct da_pipeline {
   int64_t heads = 0, heads_kv = 0, rows = 0, hg = 0, groups = 0;
   // device tensors
@@ -184,19 +192,20 @@ da_status da_pipeline_step(da_pipeline* p, const void* hq, const void* hk, const
   auto off = [](const void* base, size_t bytes) {
     return static_cast<char*>(const_cast<void*>(base)) + bytes;
   };
+  auto copy = [](void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t st,
+                 const char* what) {
+    return kCopies ? ck(cudaMemcpyAsync(dst, src, bytes, kind, st), what) : DA_OK;
+  };
   for (int64_t g = 0; g < p->groups; ++g) {
     if (p->has_prev)  // the previous call's readers of these slices
       P_TRY(ck(cudaStreamWaitEvent(p->h2d, p->comp_done[ps][g], 0), "wait"));
-    P_TRY(ck(cudaMemcpyAsync(off(p->q, g * qb), off(hq, g * qb), qb, cudaMemcpyHostToDevice,
-                             p->h2d), "h2d q"));
-    P_TRY(ck(cudaMemcpyAsync(off(p->k, g * kb), off(hk, g * kb), kb, cudaMemcpyHostToDevice,
-                             p->h2d), "h2d k"));
-    P_TRY(ck(cudaMemcpyAsync(off(p->v, g * kb), off(hv, g * kb), kb, cudaMemcpyHostToDevice,
-                             p->h2d), "h2d v"));
+    P_TRY(copy(off(p->q, g * qb), off(hq, g * qb), qb, cudaMemcpyHostToDevice, p->h2d, "h2d q"));
+    P_TRY(copy(off(p->k, g * kb), off(hk, g * kb), kb, cudaMemcpyHostToDevice, p->h2d, "h2d k"));
+    P_TRY(copy(off(p->v, g * kb), off(hv, g * kb), kb, cudaMemcpyHostToDevice, p->h2d, "h2d v"));
     P_TRY(ck(cudaEventRecord(p->fwd_ready[g], p->h2d), "event"));
     // dO is first needed by the backward: its copy overlaps the forward
-    P_TRY(ck(cudaMemcpyAsync(off(p->d_out, g * qb), off(hdo, g * qb), qb,
-                             cudaMemcpyHostToDevice, p->h2d), "h2d dO"));
+    P_TRY(copy(off(p->d_out, g * qb), off(hdo, g * qb), qb, cudaMemcpyHostToDevice, p->h2d,
+               "h2d dO"));
     P_TRY(ck(cudaEventRecord(p->in_ready[g], p->h2d), "event"));
   }
   const int64_t qr = p->hg * p->rows, kr = hgk * p->rows;  // rows of a group
@@ -253,12 +262,12 @@ da_status da_pipeline_step(da_pipeline* p, const void* hq, const void* hk, const
     P_TRY(ck(launch_convert(dv, off(p->dv16, g * kb), kr * 128, c), "convert"));
     P_TRY(ck(cudaEventRecord(p->comp_done[cs][g], c), "event"));
     P_TRY(ck(cudaStreamWaitEvent(p->d2h, p->comp_done[cs][g], 0), "wait"));
-    P_TRY(ck(cudaMemcpyAsync(off(hdq, g * qb), off(p->dq16, g * qb), qb, cudaMemcpyDeviceToHost,
-                             p->d2h), "d2h dq"));
-    P_TRY(ck(cudaMemcpyAsync(off(hdk, g * kb), off(p->dk16, g * kb), kb, cudaMemcpyDeviceToHost,
-                             p->d2h), "d2h dk"));
-    P_TRY(ck(cudaMemcpyAsync(off(hdv, g * kb), off(p->dv16, g * kb), kb, cudaMemcpyDeviceToHost,
-                             p->d2h), "d2h dv"));
+    P_TRY(copy(off(hdq, g * qb), off(p->dq16, g * qb), qb, cudaMemcpyDeviceToHost, p->d2h,
+               "d2h dq"));
+    P_TRY(copy(off(hdk, g * kb), off(p->dk16, g * kb), kb, cudaMemcpyDeviceToHost, p->d2h,
+               "d2h dk"));
+    P_TRY(copy(off(hdv, g * kb), off(p->dv16, g * kb), kb, cudaMemcpyDeviceToHost, p->d2h,
+               "d2h dv"));
     P_TRY(ck(cudaEventRecord(p->d2h_done[cs][g], p->d2h), "event"));
   }
   p->parity = ps;
