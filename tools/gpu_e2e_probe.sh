@@ -4,5 +4,5 @@ for r in 1 2; do
   timeout 120 python tools/ab_step.py $L 6 2>&1 | tail -1 | sed 's/^/device /'
   timeout 120 python tools/ab_e2e.py $L 6 2 2>&1 | tail -1 | sed 's/^/e2e /'
   timeout 120 python tools/ab_e2e.py paper_2310_03294_b200/variants/lib_nocopy.so 6 2 2>&1 | tail -1 | sed 's/^/e2e-nocopy /'
-  timeout 120 python tools/ab_e2e.py paper_2310_03294_b200/variants/lib_nocopy.so 6 32 2>&1 | tail -1 | sed 's/^/e2e-nocopy-hpg32 /'
+
 done
