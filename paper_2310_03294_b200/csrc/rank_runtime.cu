@@ -129,12 +129,19 @@ std::vector<Plan> plans_for(const FlatSchedule& s, int worker) {
 
 // Split steps as the executors implement them (make_balanced_split): a direct
 // task takes the high half of the kv rows (KVHalf payload), a helper the low
-// half of its own rows.
+// half of its own rows, and all of a worker's half tasks and half GradKVs sit
+// in one step (the half buffers and receive slots are single, not parity-
+// buffered like the whole-chunk ones).
 da_status check_parts(const std::vector<Plan>& plans) {
-  for (const Plan& p : plans)
+  int split_steps = 0;
+  for (const Plan& p : plans) {
     if ((p.action == 2 && p.part == kPartLow) || (p.action == 3 && p.part == kPartHigh))
       return set_error(DA_ERR_UNSUPPORTED,
                        "split step: direct tasks take the high half, helpers the low half");
+    if (p.part != kPartWhole || !p.kvh_sends.empty() || p.gradkv_part != kPartWhole) ++split_steps;
+  }
+  if (split_steps > 1)
+    return set_error(DA_ERR_UNSUPPORTED, "split step: at most one split step per worker");
   return DA_OK;
 }
 
