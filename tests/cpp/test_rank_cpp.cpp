@@ -114,7 +114,7 @@ int run_rank(Shared* sh, int rank, int world, int64_t n, int heads) {
     const b2::Chunk cq{dq_in.data(), heads, rows}, ck{dk_in.data(), heads, rows},
         cv{dv_in.data(), heads, rows};
     rt.forward(cq, ck, cv, out.data(), lse.data(), DA_SCHEDULE_BALANCED_SPLIT, st);
-    rt.backward(dg_in.data(), dq.data(), dk.data(), dv.data(), DA_SCHEDULE_BALANCED_BWD, st);
+    rt.backward(dg_in.data(), dq.data(), dk.data(), dv.data(), DA_SCHEDULE_BALANCED_SPLIT_BWD, st);
     const auto o16 = out.download(st);
     const auto l = lse.download(st), gq = dq.download(st), gk = dk.download(st),
                gv = dv.download(st);
@@ -124,7 +124,7 @@ int run_rank(Shared* sh, int rank, int world, int64_t n, int heads) {
       int64_t c10[10];
       dao_run_forward(world, 4, n, d, q.data() + off, k.data() + off, v.data() + off, o_r.data(),
                       l_r.data(), c10);
-      dao_run_backward_sched(world, 1, n, d, q.data() + off, k.data() + off, v.data() + off,
+      dao_run_backward_sched(world, 4, n, d, q.data() + off, k.data() + off, v.data() + off,
                              o_r.data(), l_r.data(), g.data() + off, rq.data(), rk.data(),
                              rv.data(), c10);
       std::vector<double> go, gr, qq, qr, kk, kr, vv, vr;
@@ -151,7 +151,7 @@ int run_rank(Shared* sh, int rank, int world, int64_t n, int heads) {
     }
     // deterministic runtime: a second pass repeats every bit
     rt.forward(cq, ck, cv, out.data(), lse.data(), DA_SCHEDULE_BALANCED_SPLIT, st);
-    rt.backward(dg_in.data(), dq.data(), dk.data(), dv.data(), DA_SCHEDULE_BALANCED_BWD, st);
+    rt.backward(dg_in.data(), dq.data(), dk.data(), dv.data(), DA_SCHEDULE_BALANCED_SPLIT_BWD, st);
     if (dq.download(st) != gq || dk.download(st) != gk || out.download(st) != o16) status = 3;
   } catch (const std::exception& e) {
     std::printf("rank %d: %s\n", rank, e.what());

@@ -35,7 +35,7 @@ def test_cpp_api_kernels_and_runtime(cuda):
 def test_cpp_rank_runtime_multiprocess(cuda, world):
     """tests/cpp/test_rank_cpp.cpp: W forked processes drive
     distattn::b200::RankRuntime from C++ only (shared-memory allgather
-    bootstrap, IPC transport, split forward + balanced backward, deterministic);
+    bootstrap, IPC transport, split forward + split backward, deterministic);
     each rank's chunk matches the C oracle and a second pass repeats its bits."""
     exe = EXE.parent / "test_rank_cpp"
     if not exe.exists():
