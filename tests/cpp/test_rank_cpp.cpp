@@ -3,8 +3,8 @@
 // over the C ABI), exactly as a C++ host would embed it. The bootstrap
 // allgather the runtime asks for is implemented here over a shared-memory
 // region (any transport works: MPI_Allgather, a TCP store, ...). The ranks
-// share one GPU (the IPC transport), run the balanced forward and balanced
-// backward, and each checks its chunk of O / LSE / dQ / dK / dV against the C
+// share one GPU (the IPC transport), run the balanced forward and backward
+// with the even-P split, and each checks its chunk of O / LSE / dQ / dK / dV against the C
 // oracle's stepper executors (the bit-exact restatement of the reference).
 //
 //   tests/cpp/_build/test_rank_cpp [world] [n] [heads]
