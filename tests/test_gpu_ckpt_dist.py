@@ -80,8 +80,8 @@ def _rel(a, b):
     return float((a.float() - b.float()).abs().max() / b.float().abs().max().clamp_min(1e-30))
 
 
-@pytest.mark.parametrize("world,fwd,bwd", [(2, "balanced", "ring"), (4, "balanced_split",
-                                                                      "balanced")])
+@pytest.mark.parametrize("world,fwd,bwd", [(2, "balanced", "ring"),
+                                           (4, "balanced_split", "balanced_split")])
 def test_checkpointed_layer_with_sequence_parallel_attention(cuda, world, fwd, bwd):
     from paper_2310_03294_b200 import ckptplan as K
     with tempfile.TemporaryDirectory() as td:
