@@ -406,6 +406,16 @@ inline Schedule build_balanced_schedule(int workers) {
 inline Schedule build_balanced_split_schedule(int workers) {
   return build_schedule(workers, DA_SCHEDULE_BALANCED_SPLIT);
 }
+/// Backward schedules (extensions; the reference's backward is the ring order).
+inline Schedule build_ring_backward_schedule(int workers) {
+  return build_schedule(workers, DA_SCHEDULE_RING_BWD);
+}
+inline Schedule build_balanced_backward_schedule(int workers) {
+  return build_schedule(workers, DA_SCHEDULE_BALANCED_BWD);
+}
+inline Schedule build_balanced_split_backward_schedule(int workers) {
+  return build_schedule(workers, DA_SCHEDULE_BALANCED_SPLIT_BWD);
+}
 
 inline void flatten(const Schedule& s, std::vector<int32_t>& t, std::vector<int32_t>& m) {
   t.clear();

@@ -85,7 +85,9 @@ int dao_block_attn_backward_with_d(const double* q, int64_t rq, const double* k,
                                    const double* d_out, int mask, double scale, int64_t block_rows,
                                    int64_t block_cols, double* dq, double* dk, double* dv);
 
-/* Backward over an explicit schedule table (kind 0 ring, 1 balanced):
+/* Backward over an explicit schedule table (kind 0 ring, 1 balanced, 4 the
+ * balanced schedule with the even-P split; a split step's tasks use the kv row
+ * window of their part, and a split direct pair's GradKV covers its half):
  * EXTENSION, the reference has only the ring order. Local/direct tasks follow
  * runtime.cpp:605-651 (dq += immediately, GradKV folded at the end of the step
  * in ascending receiver order); a helper h for owner o computes the pair

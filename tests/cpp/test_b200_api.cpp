@@ -215,7 +215,8 @@ static void gpu_tests() {
   for (int kind : {0, 1, 4}) {
     const std::string name = std::string("P=4 N=2048 H=2 forward (") +
                              (kind == 0 ? "ring" : kind == 1 ? "balanced" : "split") +
-                             ") + ring backward vs the oracle stepper, counters exact";
+                             ") + " + (kind == 4 ? "split (Schedule object)" : "ring") +
+                             " backward vs the oracle stepper, counters exact";
     run(name.c_str(), [&, kind] {
       const int P = 4;
       const int64_t n = 2048, d = 128, H = 2;
@@ -230,7 +231,10 @@ static void gpu_tests() {
       }
       auto shards = b2::make_shards(P, n, H, qb, kb, vb, gb, st);
       const auto cf = b2::run_forward(shards, H, static_cast<da_schedule_kind>(kind), st);
-      const auto cb = b2::run_backward(shards, H, DA_SCHEDULE_RING_BWD, st);
+      const auto cb =
+          kind == 4 ? b2::run_backward(shards, H, b2::build_balanced_split_backward_schedule(P),
+                                       b2::RunOptions{}, st)
+                    : b2::run_backward(shards, H, DA_SCHEDULE_RING_BWD, st);
       const int64_t rows = n / P;
       for (int64_t h = 0; h < H; ++h) {
         const size_t off = h * n * d;
@@ -238,8 +242,13 @@ static void gpu_tests() {
         int64_t c10[10], b10[10];
         dao_run_forward(P, kind, n, d, q.data() + off, k.data() + off, v.data() + off, o.data(),
                         lse.data(), c10);
-        dao_run_backward(P, n, d, q.data() + off, k.data() + off, v.data() + off, o.data(),
-                         lse.data(), g.data() + off, rq.data(), rk.data(), rv.data(), b10);
+        if (kind == 4)  // the oracle over the same split backward table
+          dao_run_backward_sched(P, 4, n, d, q.data() + off, k.data() + off, v.data() + off,
+                                 o.data(), lse.data(), g.data() + off, rq.data(), rk.data(),
+                                 rv.data(), b10);
+        else
+          dao_run_backward(P, n, d, q.data() + off, k.data() + off, v.data() + off, o.data(),
+                           lse.data(), g.data() + off, rq.data(), rk.data(), rv.data(), b10);
         std::vector<double> go(n * d), gl(n), gq(n * d), gk(n * d), gv(n * d);
         for (int p = 0; p < P; ++p) {
           const auto so = shards[p].out.download(st);
